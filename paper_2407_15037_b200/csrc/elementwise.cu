@@ -1,0 +1,482 @@
+// elementwise.cu -- CodedArray-level quantize / reconstruct, the NOA range
+// pass, exhaustive / sampled sweeps and the device corpus generators, sm_100a.
+//
+// Memory-bound streaming kernels: every warp moves 512 contiguous values per
+// step, each lane four consecutive values per row (one 128-bit LDG for f32,
+// two for f64), four rows per lane, so every load / store instruction of a
+// warp covers one contiguous 512 B (f32) or 1 KB (f64) span and the lossless
+// flags go out as one coalesced 128 B store per row.  Grids are sized to the
+// resident-CTA capacity of the 148 SMs and grid-stride over 4096-value tiles.
+#include "gebq_common.cuh"
+#include "gebq_internal.cuh"
+
+namespace gebq {
+
+// ---------------------------------------------------------------------------
+// vector helpers: 4 consecutive values of width U
+// ---------------------------------------------------------------------------
+template <typename U> struct Vec4;
+template <> struct Vec4<uint32_t> {
+    __device__ __forceinline__ static void load(const uint32_t *p, uint32_t v[4]) {
+        uint4 a = __ldcs(reinterpret_cast<const uint4 *>(p));
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    }
+    __device__ __forceinline__ static void store(uint32_t *p, const uint32_t v[4]) {
+        __stcs(reinterpret_cast<uint4 *>(p), make_uint4(v[0], v[1], v[2], v[3]));
+    }
+};
+template <> struct Vec4<uint64_t> {
+    __device__ __forceinline__ static void load(const uint64_t *p, uint64_t v[4]) {
+        ulonglong2 a = __ldcs(reinterpret_cast<const ulonglong2 *>(p));
+        ulonglong2 b = __ldcs(reinterpret_cast<const ulonglong2 *>(p) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    }
+    __device__ __forceinline__ static void store(uint64_t *p, const uint64_t v[4]) {
+        __stcs(reinterpret_cast<ulonglong2 *>(p), make_ulonglong2(v[0], v[1]));
+        __stcs(reinterpret_cast<ulonglong2 *>(p) + 1, make_ulonglong2(v[2], v[3]));
+    }
+};
+
+__device__ __forceinline__ void flush_trig(uint32_t t0, uint32_t t1, uint32_t t2, uint32_t t3,
+                                           unsigned long long *trig) {
+    __shared__ unsigned long long s_trig[4];
+    if (threadIdx.x < 4) s_trig[threadIdx.x] = 0;
+    __syncthreads();
+    t0 = __reduce_add_sync(0xFFFFFFFFu, t0);
+    t1 = __reduce_add_sync(0xFFFFFFFFu, t1);
+    t2 = __reduce_add_sync(0xFFFFFFFFu, t2);
+    t3 = __reduce_add_sync(0xFFFFFFFFu, t3);
+    if ((threadIdx.x & 31) == 0) {
+        if (t0) atomicAdd(&s_trig[0], (unsigned long long)t0);
+        if (t1) atomicAdd(&s_trig[1], (unsigned long long)t1);
+        if (t2) atomicAdd(&s_trig[2], (unsigned long long)t2);
+        if (t3) atomicAdd(&s_trig[3], (unsigned long long)t3);
+    }
+    __syncthreads();
+    if (threadIdx.x < 4 && s_trig[threadIdx.x]) atomicAdd(&trig[threadIdx.x], s_trig[threadIdx.x]);
+}
+
+// ---------------------------------------------------------------------------
+// quantize: (bits) -> (codes, lossless flags, 4 trigger counters)
+// replaces quantize_{abs,rel}{32,64} (_kernels.py:86-285)
+// ---------------------------------------------------------------------------
+template <typename T, int kMode, bool kUnsafe>
+__global__ void __launch_bounds__(kThreads) k_quantize(const typename W<T>::U *__restrict__ x,
+                                                       typename W<T>::U *__restrict__ codes,
+                                                       uint8_t *__restrict__ flags, int64_t n,
+                                                       Consts<T> k, const Consts<T> *kdev,
+                                                       unsigned long long *trig, int vec_ok) {
+    using U = typename W<T>::U;
+    if (kdev) k = *kdev;  // NOA: constants derived on device from the global range
+    uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+    auto count = [&](int tr) {
+        c0 += tr == TRIG_NAN; c1 += tr == TRIG_INF; c2 += tr == TRIG_GUARD; c3 += tr == TRIG_DCHECK;
+    };
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t ntiles = vec_ok ? n / kTile : 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t base = tile * kTile + warp * (kTile / kWarps) + 4 * lane;
+        U v[kRows][4];
+#pragma unroll
+        for (int r = 0; r < kRows; r++) Vec4<U>::load(x + base + 128 * r, v[r]);
+#pragma unroll
+        for (int r = 0; r < kRows; r++) {
+            uint32_t fl = 0;
+#pragma unroll
+            for (int s = 0; s < 4; s++) {
+                U c;
+                int tr = quantize_one<T, kMode, kUnsafe>(v[r][s], k, c);
+                v[r][s] = c;
+                fl |= (uint32_t)(tr != TRIG_NONE) << (8 * s);
+                count(tr);
+            }
+            Vec4<U>::store(codes + base + 128 * r, v[r]);
+            __stcs(reinterpret_cast<uint32_t *>(flags + base + 128 * r), fl);
+        }
+    }
+    // scalar tail (or everything when the pointers are not 16 B aligned)
+    const int64_t start = ntiles * kTile;
+    for (int64_t i = start + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        U c;
+        int tr = quantize_one<T, kMode, kUnsafe>(x[i], k, c);
+        codes[i] = c;
+        flags[i] = tr != TRIG_NONE;
+        count(tr);
+    }
+    flush_trig(c0, c1, c2, c3, trig);
+}
+
+// ---------------------------------------------------------------------------
+// reconstruct: (codes, flags) -> value bits; replaces reconstruct_* (_kernels.py:293-354)
+// ---------------------------------------------------------------------------
+template <typename T, int kMode>
+__global__ void __launch_bounds__(kThreads) k_reconstruct(const typename W<T>::U *__restrict__ codes,
+                                                          const uint8_t *__restrict__ flags,
+                                                          typename W<T>::U *__restrict__ out,
+                                                          int64_t n, T derived, int vec_ok) {
+    using U = typename W<T>::U;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t ntiles = vec_ok ? n / kTile : 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t base = tile * kTile + warp * (kTile / kWarps) + 4 * lane;
+        U v[kRows][4];
+        uint32_t fl[kRows];
+#pragma unroll
+        for (int r = 0; r < kRows; r++) {
+            Vec4<U>::load(codes + base + 128 * r, v[r]);
+            fl[r] = __ldcs(reinterpret_cast<const uint32_t *>(flags + base + 128 * r));
+        }
+#pragma unroll
+        for (int r = 0; r < kRows; r++) {
+#pragma unroll
+            for (int s = 0; s < 4; s++)
+                v[r][s] = reconstruct_one<T, kMode>(v[r][s], (fl[r] >> (8 * s)) & 0xFF, derived);
+            Vec4<U>::store(out + base + 128 * r, v[r]);
+        }
+    }
+    const int64_t start = ntiles * kTile;
+    for (int64_t i = start + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = reconstruct_one<T, kMode>(codes[i], flags[i] != 0, derived);
+}
+
+// ---------------------------------------------------------------------------
+// NOA range pass (compute_noa_range, quantizers.py:337-351).
+// Finite values map to order-preserving integer keys (total order, -0 < +0);
+// keys2[0] = max key, keys2[1] = max of the complemented key (= min), both as
+// signed int64 so one MAX allreduce combines shards.  0 / INT64_MIN = none.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t order_key(uint32_t b) { return (b & 0x80000000u) ? ~b : (b | 0x80000000u); }
+__device__ __forceinline__ uint64_t order_key(uint64_t b) {
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_noa_minmax(const typename W<T>::U *__restrict__ x,
+                                                         int64_t n, long long *keys2, int vec_ok) {
+    using X = W<T>;
+    using U = typename X::U;
+    U kmax = 0, kmin_c = 0;  // 0 = no finite value seen
+    auto acc = [&](U b) {
+        if (((b >> X::kMantBits) & X::kExpAll) == X::kExpAll) return;  // NaN / Inf skipped
+        U key = order_key(b);
+        kmax = key > kmax ? key : kmax;
+        kmin_c = (U)~key > kmin_c ? (U)~key : kmin_c;
+    };
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t ntiles = vec_ok ? n / kTile : 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t base = tile * kTile + warp * (kTile / kWarps) + 4 * lane;
+        U v[kRows][4];
+#pragma unroll
+        for (int r = 0; r < kRows; r++) Vec4<U>::load(x + base + 128 * r, v[r]);
+#pragma unroll
+        for (int r = 0; r < kRows; r++)
+#pragma unroll
+            for (int s = 0; s < 4; s++) acc(v[r][s]);
+    }
+    for (int64_t i = ntiles * kTile + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        acc(x[i]);
+    long long a, b;
+    if constexpr (sizeof(T) == 4) {
+        a = __reduce_max_sync(0xFFFFFFFFu, (unsigned)kmax);
+        b = __reduce_max_sync(0xFFFFFFFFu, (unsigned)kmin_c);
+    } else {
+        for (int off = 16; off; off >>= 1) {
+            U o1 = __shfl_xor_sync(0xFFFFFFFFu, kmax, off);
+            U o2 = __shfl_xor_sync(0xFFFFFFFFu, kmin_c, off);
+            kmax = o1 > kmax ? o1 : kmax;
+            kmin_c = o2 > kmin_c ? o2 : kmin_c;
+        }
+        a = (long long)(kmax ^ 0x8000000000000000ull);
+        b = (long long)(kmin_c ^ 0x8000000000000000ull);
+    }
+    if (lane == 0) {
+        atomicMax(&keys2[0], a);
+        atomicMax(&keys2[1], b);
+    }
+}
+
+// R = max - min in the value width (+0 when no finite values), then the NOA
+// constants eb_eff = f(eb)*R, eb2 = eb_eff+eb_eff, inv_eb2 = 1/eb2
+// (quantizers.py:106-116).  range_out = R widened to f64 (the header's range_bits).
+template <typename T>
+__global__ void k_noa_derive(const long long *keys2, double eb, Consts<T> *kout, double *range_out) {
+    using X = W<T>;
+    using U = typename X::U;
+    U kmax, kmin_c;
+    if constexpr (sizeof(T) == 4) {
+        kmax = (U)keys2[0];
+        kmin_c = (U)keys2[1];
+    } else {
+        kmax = (U)keys2[0] ^ 0x8000000000000000ull;
+        kmin_c = (U)keys2[1] ^ 0x8000000000000000ull;
+    }
+    T R = T(0);
+    if (kmax != 0) {
+        const U top = (U)1 << (X::kBits - 1);
+        U kmin = ~kmin_c;
+        U bmax = (kmax & top) ? (kmax & ~top) : ~kmax;
+        U bmin = (kmin & top) ? (kmin & ~top) : ~kmin;
+        R = X::sub(X::from_bits(bmax), X::from_bits(bmin));
+    }
+    T eps_w;
+    if constexpr (sizeof(T) == 4) eps_w = __double2float_rn(eb); else eps_w = eb;
+    T eb_eff = X::mul(eps_w, R);
+    T eb2 = X::add(eb_eff, eb_eff);
+    Consts<T> k;
+    k.a = eb_eff;
+    k.b = eb2;
+    k.c = X::div(T(1), eb2);
+    k.thr = (T)(X::kMaxBin - 1);
+    *kout = k;
+    *range_out = (double)R;
+}
+
+// ---------------------------------------------------------------------------
+// sweeps: quantize -> reconstruct -> check, tallied per value class
+// (sweep_*_on, _kernels.py:717-896).  Patterns come from the index (range),
+// an explicit array, or splitmix64 -- no HBM traffic for the first and last.
+// Counters: 15 x 16-bit lanes packed in 4 u64 registers (host bounds the
+// per-thread pattern count below 2^16).
+// ---------------------------------------------------------------------------
+template <typename T, int kMode, bool kUnsafe>
+__device__ __forceinline__ int sweep_outcome(typename W<T>::U xb, const Consts<T> &k) {
+    using X = W<T>;
+    using U = typename X::U;
+    T xf = X::from_bits(xb);
+    if constexpr (kMode == MODE_ABS) {
+        if (xf != xf) return 1;
+        T t = X::mul(xf, k.c);
+        if (!(X::fabs_(t) < k.thr)) return 1;
+        T bf;
+        int64_t b = round_bin(t, bf);
+        if (b >= X::kMaxBin || b <= -X::kMaxBin) return 1;
+        T recon = X::mul(bf, k.b);
+        T err = X::fabs_(X::sub(xf, recon));
+        if (!kUnsafe && !(err <= k.a)) return 1;
+        return err <= k.a ? 0 : 2;
+    } else {
+        U ab = xb & X::kAbsMask;
+        int64_t aexpo = (int64_t)(ab >> X::kMantBits);
+        if (xf != xf || aexpo == (int64_t)X::kExpAll || aexpo == 0) return 1;
+        T frac = X::from_bits(((U)X::kBias << X::kMantBits) | (ab & X::kMantMask));
+        T l = X::add(frac, (T)(aexpo - (X::kBias + 1)));
+        T t = X::div(l, k.b);
+        if (!(X::fabs_(t) < k.thr)) return 1;
+        T kf;
+        int64_t kb = round_bin(t, kf);
+        if (kb >= X::kMaxBin || kb <= -X::kMaxBin) return 1;
+        T p = X::mul(kf, k.b);
+        T biased = X::add(p, (T)X::kBias);
+        if (!(biased >= T(1) && biased < (T)(2 * X::kBias + 1))) return 1;
+        int64_t expo = X::trunc_i64(biased);
+        T rfrac = X::sub(biased, (T)(expo - 1));
+        T recon_mag = pow2_assemble<T>(expo, rfrac);
+        T q = X::div(recon_mag, X::fabs_(xf));
+        bool ok = q <= k.a && X::mul(q, k.a) >= T(1);
+        if (!kUnsafe && !ok) return 1;
+        return ok ? 0 : 2;
+    }
+}
+
+struct Tally16 {
+    uint64_t r[4] = {0, 0, 0, 0};
+    __device__ __forceinline__ void add(int key) {
+        uint64_t inc = 1ull << (16 * (key & 3));
+        int w = key >> 2;
+        r[0] += w == 0 ? inc : 0;
+        r[1] += w == 1 ? inc : 0;
+        r[2] += w == 2 ? inc : 0;
+        r[3] += w == 3 ? inc : 0;
+    }
+    __device__ __forceinline__ void flush(unsigned long long *tally15) {
+#pragma unroll
+        for (int key = 0; key < 15; key++) {
+            uint32_t v = (uint32_t)((r[key >> 2] >> (16 * (key & 3))) & 0xFFFF);
+            v = __reduce_add_sync(0xFFFFFFFFu, v);
+            if ((threadIdx.x & 31) == 0 && v) atomicAdd(&tally15[key], (unsigned long long)v);
+        }
+    }
+};
+
+// kSource: 0 = index range (bits = start + i mod 2^32), 1 = explicit array,
+// 2 = splitmix64(seed, start + i + 1) (low 32 bits for f32)
+template <typename T, int kMode, bool kUnsafe, int kSource>
+__global__ void __launch_bounds__(kThreads) k_sweep(uint64_t start, int64_t count,
+                                                    const typename W<T>::U *__restrict__ bits,
+                                                    uint64_t seed, Consts<T> k,
+                                                    unsigned long long *tally15,
+                                                    unsigned long long *first_viol,
+                                                    int64_t idx_base) {
+    using U = typename W<T>::U;
+    Tally16 tl;
+    uint64_t first = ~0ull;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+#pragma unroll 4
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+        U xb;
+        if constexpr (kSource == 0) xb = (U)(start + (uint64_t)i);
+        else if constexpr (kSource == 1) xb = bits[i];
+        else xb = (U)splitmix64_at(seed, start + (uint64_t)i + 1);
+        int o = sweep_outcome<T, kMode, kUnsafe>(xb, k);
+        tl.add(value_class<T>(xb) * 3 + o);
+        if (o == 2 && (uint64_t)i < first) first = (uint64_t)i;
+    }
+    tl.flush(tally15);
+    if (first != ~0ull) atomicMin(first_viol, (unsigned long long)(idx_base + (int64_t)first));
+}
+
+// ---------------------------------------------------------------------------
+// device corpus generators (splitmix64_fill, _kernels.py:671-685; C2 recipe)
+// ---------------------------------------------------------------------------
+__global__ void k_splitmix64_fill(uint64_t *out, int64_t n, uint64_t seed, int64_t start_index) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = splitmix64_at(seed, (uint64_t)(start_index + i + 1));
+}
+
+// mixed-class f32 patterns from one splitmix64 word each
+__global__ void k_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_index) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t w = splitmix64_at(seed, (uint64_t)(start_index + i + 1));
+        uint32_t sel = (uint32_t)(w >> 56);
+        uint32_t sign = (uint32_t)((w >> 55) & 1) << 31;
+        uint32_t lo = (uint32_t)w;
+        uint32_t mant = lo & 0x7FFFFFu;
+        uint32_t b;
+        if (sel < 4) b = sign | 0x7F800000u | (mant | 1u);
+        else if (sel < 8) b = sign | 0x7F800000u;
+        else if (sel < 12) b = sign | mant;
+        else if (sel < 16) b = sign | (0x7F7FFF00u + (lo & 0xFFu));
+        else b = sign | ((107u + (uint32_t)((w >> 32) % 41u)) << 23) | mant;
+        out[i] = b;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers (called from capi.cu)
+// ---------------------------------------------------------------------------
+template <typename T>
+int launch_quantize(int mode, const void *x, void *codes, uint8_t *flags, int64_t n,
+                    const Consts<T> &k, const Consts<T> *kdev, int unsafe,
+                    unsigned long long *trig, cudaStream_t st) {
+    using U = typename W<T>::U;
+    int vec = aligned16(x) && aligned16(codes) && aligned16(flags);
+    int grid = grid_for(n);
+    auto *xp = (const U *)x;
+    auto *cp = (U *)codes;
+    if (mode == MODE_REL) {
+        if (unsafe) k_quantize<T, MODE_REL, true><<<grid, kThreads, 0, st>>>(xp, cp, flags, n, k, kdev, trig, vec);
+        else k_quantize<T, MODE_REL, false><<<grid, kThreads, 0, st>>>(xp, cp, flags, n, k, kdev, trig, vec);
+    } else {
+        if (unsafe) k_quantize<T, MODE_ABS, true><<<grid, kThreads, 0, st>>>(xp, cp, flags, n, k, kdev, trig, vec);
+        else k_quantize<T, MODE_ABS, false><<<grid, kThreads, 0, st>>>(xp, cp, flags, n, k, kdev, trig, vec);
+    }
+    return check_launch("quantize");
+}
+template int launch_quantize<float>(int, const void *, void *, uint8_t *, int64_t, const Consts<float> &,
+                                    const Consts<float> *, int, unsigned long long *, cudaStream_t);
+template int launch_quantize<double>(int, const void *, void *, uint8_t *, int64_t, const Consts<double> &,
+                                     const Consts<double> *, int, unsigned long long *, cudaStream_t);
+
+template <typename T>
+int launch_reconstruct(int mode, const void *codes, const uint8_t *flags, void *out, int64_t n,
+                       T derived, cudaStream_t st) {
+    using U = typename W<T>::U;
+    int vec = aligned16(codes) && aligned16(out) && aligned16(flags);
+    int grid = grid_for(n);
+    if (mode == MODE_REL)
+        k_reconstruct<T, MODE_REL><<<grid, kThreads, 0, st>>>((const U *)codes, flags, (U *)out, n, derived, vec);
+    else
+        k_reconstruct<T, MODE_ABS><<<grid, kThreads, 0, st>>>((const U *)codes, flags, (U *)out, n, derived, vec);
+    return check_launch("reconstruct");
+}
+template int launch_reconstruct<float>(int, const void *, const uint8_t *, void *, int64_t, float, cudaStream_t);
+template int launch_reconstruct<double>(int, const void *, const uint8_t *, void *, int64_t, double, cudaStream_t);
+
+template <typename T>
+int launch_noa_minmax(const void *x, int64_t n, long long *keys2, cudaStream_t st) {
+    using U = typename W<T>::U;
+    cudaError_t e = cudaMemsetAsync(keys2, 0, 2 * sizeof(long long), st);
+    if (e != cudaSuccess) return set_error(e, "noa memset");
+    if constexpr (sizeof(T) == 8) {
+        // "none" for the signed-int64 view of f64 keys is INT64_MIN
+        static const long long none[2] = {(long long)0x8000000000000000ull, (long long)0x8000000000000000ull};
+        e = cudaMemcpyAsync(keys2, none, sizeof(none), cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return set_error(e, "noa init");
+    }
+    int grid = grid_for(n);
+    k_noa_minmax<T><<<grid, kThreads, 0, st>>>((const U *)x, n, keys2, aligned16(x));
+    return check_launch("noa_minmax");
+}
+template int launch_noa_minmax<float>(const void *, int64_t, long long *, cudaStream_t);
+template int launch_noa_minmax<double>(const void *, int64_t, long long *, cudaStream_t);
+
+template <typename T>
+int launch_noa_derive(const long long *keys2, double eb, Consts<T> *kout, double *range_out,
+                      cudaStream_t st) {
+    k_noa_derive<T><<<1, 1, 0, st>>>(keys2, eb, kout, range_out);
+    return check_launch("noa_derive");
+}
+template int launch_noa_derive<float>(const long long *, double, Consts<float> *, double *, cudaStream_t);
+template int launch_noa_derive<double>(const long long *, double, Consts<double> *, double *, cudaStream_t);
+
+template <typename T, int kMode, bool kUnsafe>
+static void sweep_dispatch(int source, int grid, uint64_t start, int64_t count, const void *bits,
+                           uint64_t seed, const Consts<T> &k, unsigned long long *tally15,
+                           unsigned long long *first, int64_t idx_base, cudaStream_t st) {
+    using U = typename W<T>::U;
+    if (source == 0)
+        k_sweep<T, kMode, kUnsafe, 0><<<grid, kThreads, 0, st>>>(start, count, (const U *)bits, seed, k, tally15, first, idx_base);
+    else if (source == 1)
+        k_sweep<T, kMode, kUnsafe, 1><<<grid, kThreads, 0, st>>>(start, count, (const U *)bits, seed, k, tally15, first, idx_base);
+    else
+        k_sweep<T, kMode, kUnsafe, 2><<<grid, kThreads, 0, st>>>(start, count, (const U *)bits, seed, k, tally15, first, idx_base);
+}
+
+// tally15 / first_viol are device buffers (zero / all-ones on entry); the
+// first-violation slot receives the sequence index of the first failing pattern.
+template <typename T>
+int launch_sweep(int mode, int unsafe, int source, uint64_t start, int64_t count, const void *bits,
+                 uint64_t seed, const Consts<T> &k, unsigned long long *tally15,
+                 unsigned long long *first, cudaStream_t st) {
+    // Split so each thread handles < 2^16 patterns per launch (16-bit packed counters).
+    const int grid = resident_grid();
+    const int64_t per_launch = (int64_t)grid * kThreads * 60000;
+    for (int64_t off = 0; off < count; off += per_launch) {
+        int64_t c = count - off < per_launch ? count - off : per_launch;
+        const void *b = source == 1 ? (const void *)((const char *)bits + off * sizeof(typename W<T>::U)) : bits;
+        uint64_t s = start + (uint64_t)off;
+        if (mode == MODE_REL) {
+            if (unsafe) sweep_dispatch<T, MODE_REL, true>(source, grid, s, c, b, seed, k, tally15, first, off, st);
+            else sweep_dispatch<T, MODE_REL, false>(source, grid, s, c, b, seed, k, tally15, first, off, st);
+        } else {
+            if (unsafe) sweep_dispatch<T, MODE_ABS, true>(source, grid, s, c, b, seed, k, tally15, first, off, st);
+            else sweep_dispatch<T, MODE_ABS, false>(source, grid, s, c, b, seed, k, tally15, first, off, st);
+        }
+        int rc = check_launch("sweep");
+        if (rc) return rc;
+    }
+    return 0;
+}
+template int launch_sweep<float>(int, int, int, uint64_t, int64_t, const void *, uint64_t, const Consts<float> &,
+                                 unsigned long long *, unsigned long long *, cudaStream_t);
+template int launch_sweep<double>(int, int, int, uint64_t, int64_t, const void *, uint64_t, const Consts<double> &,
+                                  unsigned long long *, unsigned long long *, cudaStream_t);
+
+int64_t sweep_per_launch() { return (int64_t)resident_grid() * kThreads * 60000; }
+
+int launch_splitmix64_fill(uint64_t *out, int64_t n, uint64_t seed, int64_t start_index, cudaStream_t st) {
+    k_splitmix64_fill<<<grid_for(n), kThreads, 0, st>>>(out, n, seed, start_index);
+    return check_launch("splitmix64_fill");
+}
+int launch_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_index, cudaStream_t st) {
+    k_gen_mixed_f32<<<grid_for(n), kThreads, 0, st>>>(out, n, seed, start_index);
+    return check_launch("gen_mixed_f32");
+}
+
+}  // namespace gebq

@@ -1,0 +1,55 @@
+// gebq_internal.cuh -- launch geometry, error plumbing and launcher
+// declarations shared by the kernel files and the C-ABI (capi.cu).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "gebq_common.cuh"
+
+namespace gebq {
+
+constexpr int kThreads = 256;                  // 8 warps per CTA
+constexpr int kWarps = kThreads / 32;
+constexpr int kRows = 4;                       // rows of 128 values per lane-tile
+constexpr int kTile = kThreads * 4 * kRows;    // 4096 values per CTA step
+
+inline bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+// error state (thread-local text, returned codes are negative)
+int set_error(cudaError_t e, const char *what);
+int set_error_msg(int code, const char *msg);
+int check_launch(const char *what);
+
+// SM count x resident CTAs of kThreads (queried once per device)
+int sm_count();
+int resident_grid();
+inline int grid_for(int64_t n) {
+    int64_t tiles = (n + kTile - 1) / kTile;
+    int g = resident_grid();
+    if (tiles < 1) tiles = 1;
+    return (int)(tiles < g ? tiles : g);
+}
+
+template <typename T>
+int launch_quantize(int mode, const void *x, void *codes, uint8_t *flags, int64_t n,
+                    const Consts<T> &k, const Consts<T> *kdev, int unsafe,
+                    unsigned long long *trig, cudaStream_t st);
+template <typename T>
+int launch_reconstruct(int mode, const void *codes, const uint8_t *flags, void *out, int64_t n,
+                       T derived, cudaStream_t st);
+template <typename T>
+int launch_noa_minmax(const void *x, int64_t n, long long *keys2, cudaStream_t st);
+template <typename T>
+int launch_noa_derive(const long long *keys2, double eb, Consts<T> *kout, double *range_out,
+                      cudaStream_t st);
+template <typename T>
+int launch_sweep(int mode, int unsafe, int source, uint64_t start, int64_t count, const void *bits,
+                 uint64_t seed, const Consts<T> &k, unsigned long long *tally15,
+                 unsigned long long *first, cudaStream_t st);
+int launch_splitmix64_fill(uint64_t *out, int64_t n, uint64_t seed, int64_t start_index,
+                           cudaStream_t st);
+int launch_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_index,
+                         cudaStream_t st);
+
+}  // namespace gebq

@@ -1,0 +1,83 @@
+"""Synthetic inputs for the BASELINE.json configurations.
+
+Host (numpy) recipes are the normative definitions; the device generators in
+``device.py`` reproduce the integer-only recipes bit-for-bit on the GPU so
+that 2^26..2^30-element inputs never have to cross PCIe.
+
+* C1 -- ABS f32 eb=1e-3, 256^3 smooth field:
+  x[i,j,k] = f32(5 sin(2 pi i/256) cos(2 pi j/256) sin(2 pi k/128) + 0.02 z),
+  z = default_rng(0).standard_normal((256,)*3), f64 math then one cast.
+* C2 -- REL f32 eb=1e-2, 2^26 mixed values, integer-only splitmix64 recipe
+  (seed 0x5EED0002); exercises every outlier path.
+* C3 -- NOA f32 eb=1e-4, 2^30 values: the 1024^3 version of the C1 formula
+  (periods 1024/1024/512) with planted NaN/+Inf and min -7 / max +7 at the two
+  ends so the range needs the global reduction.
+* C5 -- f64: (i) raw splitmix64 words, seed 0x5EED0005; (ii) the smooth field.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+C2_SEED = 0x5EED0002
+C5_SEED = 0x5EED0005
+
+
+def splitmix64(n: int, seed: int, start_index: int = 0) -> np.ndarray:
+    """splitmix64 output numbers start_index+1 .. start_index+n (vectorised numpy).
+
+    Same recurrence as the reference's ``splitmix64_fill`` (_kernels.py:671-685).
+    """
+    with np.errstate(over="ignore"):
+        idx = np.arange(start_index + 1, start_index + n + 1, dtype=np.uint64)
+        z = np.uint64(seed) + np.uint64(0x9E3779B97F4A7C15) * idx
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def c2_bits_from_words(w: np.ndarray) -> np.ndarray:
+    """map splitmix64 words to mixed-class f32 patterns."""
+    w = w.astype(np.uint64)
+    sel = w >> np.uint64(56)
+    sign = ((w >> np.uint64(55)) & np.uint64(1)) << np.uint64(31)
+    lo = w & np.uint64(0xFFFFFFFF)
+    mant = lo & np.uint64(0x7FFFFF)
+    default = sign | ((np.uint64(107) + (w >> np.uint64(32)) % np.uint64(41)) << np.uint64(23)) | mant
+    out = default
+    out = np.where(sel < 16, sign | (np.uint64(0x7F7FFF00) + (lo & np.uint64(0xFF))), out)
+    out = np.where(sel < 12, sign | mant, out)
+    out = np.where(sel < 8, sign | np.uint64(0x7F800000), out)
+    out = np.where(sel < 4, sign | np.uint64(0x7F800000) | (mant | np.uint64(1)), out)
+    return out.astype(np.uint32)
+
+
+def c2_values(n: int = 1 << 26, seed: int = C2_SEED, start_index: int = 0) -> np.ndarray:
+    return c2_bits_from_words(splitmix64(n, seed, start_index)).view(np.float32)
+
+
+def smooth_field(side: int = 256, seed: int = 0, dtype=np.float32) -> np.ndarray:
+    """C1 (side=256) field; C3 uses side=1024 with seed 1 (host version)."""
+    rng = np.random.default_rng(seed)
+    z = rng.standard_normal((side,) * 3)
+    i = np.arange(side, dtype=np.float64)
+    a = np.sin(2 * np.pi * i / side)[:, None, None]
+    b = np.cos(2 * np.pi * i / side)[None, :, None]
+    c = np.sin(2 * np.pi * i / (side // 2))[None, None, :]
+    x = 5.0 * a * b * c + 0.02 * z
+    return x.astype(dtype).ravel()
+
+
+def plant_noa_extremes(x: np.ndarray) -> np.ndarray:
+    """C3: NaN at x[0], +Inf at x[1], global min -7 in the first block and max +7
+    in the last block, so R = 14 needs a cross-shard reduction."""
+    x = x.copy()
+    x[0] = np.nan
+    x[1] = np.inf
+    x[2] = -7.0
+    x[-1] = 7.0
+    return x
+
+
+def c5_random_values(n: int, seed: int = C5_SEED) -> np.ndarray:
+    return splitmix64(n, seed).view(np.float64)
