@@ -133,6 +133,104 @@ int gebq_splitmix64_fill(uint64_t *out, int64_t n, uint64_t seed, int64_t start_
 int gebq_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_index,
                        void *stream);
 
+
+/* ---- stream encode: quantize + pack into FORMAT.md in ONE pass ------------
+ * Replaces quantize_* + block_sizes_* + cumsum + emit_blocks_* as driven by
+ * pipeline.compress / container.encode_stream (pipeline.py:112-191,
+ * container.py:235-259, _kernels.py:439-518/606-639).
+ * Writes the block REGION (bitmaps + LEB128 varints) to `region` and the N
+ * block offsets (u64, relative to the region start, plus base_offset) to
+ * `index`; *region_len (device) receives the region byte count.  The host
+ * adds the 48-byte header and the u64 block count (container.py:258).
+ *   region capacity: gebq_encode_region_capacity(n, block_size, width) bytes
+ *   workspace:       gebq_encode_workspace_bytes(n, block_size, width) bytes
+ * base_offset lets a shard of a multi-GPU job write its part of the global
+ * index directly (shard boundaries are multiples of block_size).            */
+int64_t gebq_encode_region_capacity(int64_t n, int64_t block_size, int width);
+size_t gebq_encode_workspace_bytes(int64_t n, int64_t block_size, int width);
+int gebq_encode_abs_f32(const uint32_t *x, int64_t n, float eb_eff, float eb2, float inv_eb2,
+                        float thr, int unsafe, int64_t block_size, uint8_t *region,
+                        uint64_t *index, int64_t base_offset, void *ws, size_t ws_bytes,
+                        unsigned long long *trig4, long long *region_len, void *stream);
+int gebq_encode_abs_f64(const uint64_t *x, int64_t n, double eb_eff, double eb2, double inv_eb2,
+                        double thr, int unsafe, int64_t block_size, uint8_t *region,
+                        uint64_t *index, int64_t base_offset, void *ws, size_t ws_bytes,
+                        unsigned long long *trig4, long long *region_len, void *stream);
+int gebq_encode_rel_f32(const uint32_t *x, int64_t n, float op_eps, float w, float thr,
+                        int unsafe, int64_t block_size, uint8_t *region, uint64_t *index,
+                        int64_t base_offset, void *ws, size_t ws_bytes,
+                        unsigned long long *trig4, long long *region_len, void *stream);
+int gebq_encode_rel_f64(const uint64_t *x, int64_t n, double op_eps, double w, double thr,
+                        int unsafe, int64_t block_size, uint8_t *region, uint64_t *index,
+                        int64_t base_offset, void *ws, size_t ws_bytes,
+                        unsigned long long *trig4, long long *region_len, void *stream);
+int gebq_encode_noa_dev_f32(const uint32_t *x, int64_t n, const void *consts_dev, int unsafe,
+                            int64_t block_size, uint8_t *region, uint64_t *index,
+                            int64_t base_offset, void *ws, size_t ws_bytes,
+                            unsigned long long *trig4, long long *region_len, void *stream);
+int gebq_encode_noa_dev_f64(const uint64_t *x, int64_t n, const void *consts_dev, int unsafe,
+                            int64_t block_size, uint8_t *region, uint64_t *index,
+                            int64_t base_offset, void *ws, size_t ws_bytes,
+                            unsigned long long *trig4, long long *region_len, void *stream);
+/* encode_stream(CodedArray, header) (container.py:235-259): pack given codes */
+int gebq_encode_coded_u32(const uint32_t *codes, const uint8_t *lossless, int64_t n,
+                          int64_t block_size, uint8_t *region, uint64_t *index,
+                          int64_t base_offset, void *ws, size_t ws_bytes, long long *region_len,
+                          void *stream);
+int gebq_encode_coded_u64(const uint64_t *codes, const uint8_t *lossless, int64_t n,
+                          int64_t block_size, uint8_t *region, uint64_t *index,
+                          int64_t base_offset, void *ws, size_t ws_bytes, long long *region_len,
+                          void *stream);
+
+/* ---- stream decode --------------------------------------------------------
+ * validate_index: the index checks of decode_stream (container.py:283-291);
+ *   flags3 = {first offset != 0, offsets decreasing, last offset > region_len}.
+ * decode_{abs,rel}_*: unpack + reconstruct fused (decode_blocks_* then
+ *   reconstruct_*, pipeline.py:195-213) straight to value bits.
+ * decode_blocks_u{32,64}: decode_blocks_* (_kernels.py:642-664) to codes +
+ *   lossless flags for blocks [b0, b1).
+ * Errors: *err_key (device, caller sets UINT64_MAX) is atomically MIN-ed with
+ *   (position << 2) | status, status 1 truncated / 2 non-canonical / 3 count
+ *   mismatch (_kernels.py:33-37), position relative to the region -- the
+ *   reference reports the failure with the smallest position
+ *   (container.py:308-311).                                                  */
+int gebq_validate_index(const int64_t *offsets, int64_t nblocks, int64_t region_len,
+                        int *flags3, void *stream);
+int gebq_decode_abs_f32(const uint8_t *region, int64_t region_len, const int64_t *offsets,
+                        int64_t nblocks, int64_t count, int64_t block_size, float eb2,
+                        uint32_t *out, unsigned long long *err_key, void *stream);
+int gebq_decode_abs_f64(const uint8_t *region, int64_t region_len, const int64_t *offsets,
+                        int64_t nblocks, int64_t count, int64_t block_size, double eb2,
+                        uint64_t *out, unsigned long long *err_key, void *stream);
+int gebq_decode_rel_f32(const uint8_t *region, int64_t region_len, const int64_t *offsets,
+                        int64_t nblocks, int64_t count, int64_t block_size, float w,
+                        uint32_t *out, unsigned long long *err_key, void *stream);
+int gebq_decode_rel_f64(const uint8_t *region, int64_t region_len, const int64_t *offsets,
+                        int64_t nblocks, int64_t count, int64_t block_size, double w,
+                        uint64_t *out, unsigned long long *err_key, void *stream);
+int gebq_decode_blocks_u32(const uint8_t *buf, const int64_t *offsets, int64_t noffsets,
+                           int64_t region_end, int64_t count, int64_t block_size, int64_t b0,
+                           int64_t b1, uint32_t *codes, uint8_t *lossless,
+                           unsigned long long *err_key, void *stream);
+int gebq_decode_blocks_u64(const uint8_t *buf, const int64_t *offsets, int64_t noffsets,
+                           int64_t region_end, int64_t count, int64_t block_size, int64_t b0,
+                           int64_t b1, uint64_t *codes, uint8_t *lossless,
+                           unsigned long long *err_key, void *stream);
+
+/* ---- drop-ins for block_sizes_u{32,64} / emit_blocks_u{32,64} -------------
+ * (_kernels.py:606-639): per-block encoded sizes and emission at given
+ * offsets, blocks [b0, b1).                                                 */
+int gebq_block_sizes_u32(const uint32_t *codes, int64_t count, int64_t block_size, int64_t b0,
+                         int64_t b1, int64_t *sizes, void *stream);
+int gebq_block_sizes_u64(const uint64_t *codes, int64_t count, int64_t block_size, int64_t b0,
+                         int64_t b1, int64_t *sizes, void *stream);
+int gebq_emit_blocks_u32(const uint32_t *codes, const uint8_t *lossless, int64_t count,
+                         int64_t block_size, int64_t b0, int64_t b1, const int64_t *offsets,
+                         uint8_t *out, void *stream);
+int gebq_emit_blocks_u64(const uint64_t *codes, const uint8_t *lossless, int64_t count,
+                         int64_t block_size, int64_t b0, int64_t b1, const int64_t *offsets,
+                         uint8_t *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -50,8 +50,36 @@ SIGNATURES = {
     "gebq_sweep_rel_f64": [_int, _vp, _u64, _i64, _u64, _f64, _f64, _f64, _int, _vp, _vp, _vp],
     "gebq_splitmix64_fill": [_vp, _i64, _u64, _i64, _vp],
     "gebq_gen_mixed_f32": [_vp, _i64, _u64, _i64, _vp],
+    "gebq_encode_region_capacity": [_i64, _i64, _int],
+    "gebq_encode_workspace_bytes": [_i64, _i64, _int],
+    "gebq_encode_abs_f32": [_vp, _i64, _f32, _f32, _f32, _f32, _int, _i64, _vp, _vp, _i64, _vp,
+                            ctypes.c_size_t, _vp, _vp, _vp],
+    "gebq_encode_abs_f64": [_vp, _i64, _f64, _f64, _f64, _f64, _int, _i64, _vp, _vp, _i64, _vp,
+                            ctypes.c_size_t, _vp, _vp, _vp],
+    "gebq_encode_rel_f32": [_vp, _i64, _f32, _f32, _f32, _int, _i64, _vp, _vp, _i64, _vp,
+                            ctypes.c_size_t, _vp, _vp, _vp],
+    "gebq_encode_rel_f64": [_vp, _i64, _f64, _f64, _f64, _int, _i64, _vp, _vp, _i64, _vp,
+                            ctypes.c_size_t, _vp, _vp, _vp],
+    "gebq_encode_noa_dev_f32": [_vp, _i64, _vp, _int, _i64, _vp, _vp, _i64, _vp, ctypes.c_size_t,
+                                _vp, _vp, _vp],
+    "gebq_encode_noa_dev_f64": [_vp, _i64, _vp, _int, _i64, _vp, _vp, _i64, _vp, ctypes.c_size_t,
+                                _vp, _vp, _vp],
+    "gebq_encode_coded_u32": [_vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp, ctypes.c_size_t, _vp, _vp],
+    "gebq_encode_coded_u64": [_vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp, ctypes.c_size_t, _vp, _vp],
+    "gebq_validate_index": [_vp, _i64, _i64, _vp, _vp],
+    "gebq_decode_abs_f32": [_vp, _i64, _vp, _i64, _i64, _i64, _f32, _vp, _vp, _vp],
+    "gebq_decode_abs_f64": [_vp, _i64, _vp, _i64, _i64, _i64, _f64, _vp, _vp, _vp],
+    "gebq_decode_rel_f32": [_vp, _i64, _vp, _i64, _i64, _i64, _f32, _vp, _vp, _vp],
+    "gebq_decode_rel_f64": [_vp, _i64, _vp, _i64, _i64, _i64, _f64, _vp, _vp, _vp],
+    "gebq_decode_blocks_u32": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp],
+    "gebq_decode_blocks_u64": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp],
+    "gebq_block_sizes_u32": [_vp, _i64, _i64, _i64, _i64, _vp, _vp],
+    "gebq_block_sizes_u64": [_vp, _i64, _i64, _i64, _i64, _vp, _vp],
+    "gebq_emit_blocks_u32": [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp],
+    "gebq_emit_blocks_u64": [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp],
 }
-_RESTYPES = {"gebq_b200_last_error": ctypes.c_char_p}
+_RESTYPES = {"gebq_b200_last_error": ctypes.c_char_p, "gebq_encode_region_capacity": _i64,
+             "gebq_encode_workspace_bytes": ctypes.c_size_t}
 
 _lock = threading.Lock()
 _lib = None

@@ -6,6 +6,7 @@
 
 #include "../../include/gebq_b200.h"
 #include "gebq_internal.cuh"
+#include "gebq_stream.cuh"
 
 
 namespace gebq {
@@ -166,6 +167,154 @@ int gebq_splitmix64_fill(uint64_t *out, int64_t n, uint64_t seed, int64_t start_
 }
 int gebq_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_index, void *stream) {
     return launch_gen_mixed_f32(out, n, seed, start_index, S(stream));
+}
+
+}  // extern "C"
+
+// ---- stream encode / decode (FORMAT.md) ------------------------------------
+extern "C" {
+
+int64_t gebq_encode_region_capacity(int64_t n, int64_t block_size, int width) {
+    return encode_region_capacity(n, block_size, width);
+}
+size_t gebq_encode_workspace_bytes(int64_t n, int64_t block_size, int width) {
+    return encode_workspace_bytes(n, block_size, width);
+}
+
+#define ENC_CFG(MODE, SRC)                                                                \
+    EncodeCfg cfg{MODE, SRC, unsafe, n, block_size, base_offset};
+
+int gebq_encode_abs_f32(const uint32_t *x, int64_t n, float eb_eff, float eb2, float inv_eb2, float thr,
+                        int unsafe, int64_t block_size, uint8_t *region, uint64_t *index,
+                        int64_t base_offset, void *ws, size_t ws_bytes, unsigned long long *trig4,
+                        long long *region_len, void *stream) {
+    ENC_CFG(MODE_ABS, 0)
+    Consts<float> k{eb_eff, eb2, inv_eb2, thr};
+    return launch_encode<float>(cfg, x, nullptr, k, nullptr, region, index, ws, ws_bytes, trig4, region_len, S(stream));
+}
+int gebq_encode_abs_f64(const uint64_t *x, int64_t n, double eb_eff, double eb2, double inv_eb2, double thr,
+                        int unsafe, int64_t block_size, uint8_t *region, uint64_t *index,
+                        int64_t base_offset, void *ws, size_t ws_bytes, unsigned long long *trig4,
+                        long long *region_len, void *stream) {
+    ENC_CFG(MODE_ABS, 0)
+    Consts<double> k{eb_eff, eb2, inv_eb2, thr};
+    return launch_encode<double>(cfg, x, nullptr, k, nullptr, region, index, ws, ws_bytes, trig4, region_len, S(stream));
+}
+int gebq_encode_rel_f32(const uint32_t *x, int64_t n, float op_eps, float w, float thr, int unsafe,
+                        int64_t block_size, uint8_t *region, uint64_t *index, int64_t base_offset,
+                        void *ws, size_t ws_bytes, unsigned long long *trig4, long long *region_len,
+                        void *stream) {
+    ENC_CFG(MODE_REL, 0)
+    Consts<float> k{op_eps, w, 0.0f, thr};
+    return launch_encode<float>(cfg, x, nullptr, k, nullptr, region, index, ws, ws_bytes, trig4, region_len, S(stream));
+}
+int gebq_encode_rel_f64(const uint64_t *x, int64_t n, double op_eps, double w, double thr, int unsafe,
+                        int64_t block_size, uint8_t *region, uint64_t *index, int64_t base_offset,
+                        void *ws, size_t ws_bytes, unsigned long long *trig4, long long *region_len,
+                        void *stream) {
+    ENC_CFG(MODE_REL, 0)
+    Consts<double> k{op_eps, w, 0.0, thr};
+    return launch_encode<double>(cfg, x, nullptr, k, nullptr, region, index, ws, ws_bytes, trig4, region_len, S(stream));
+}
+int gebq_encode_noa_dev_f32(const uint32_t *x, int64_t n, const void *consts_dev, int unsafe,
+                            int64_t block_size, uint8_t *region, uint64_t *index, int64_t base_offset,
+                            void *ws, size_t ws_bytes, unsigned long long *trig4, long long *region_len,
+                            void *stream) {
+    ENC_CFG(MODE_ABS, 0)
+    Consts<float> k{};
+    return launch_encode<float>(cfg, x, nullptr, k, (const Consts<float> *)consts_dev, region, index, ws,
+                                ws_bytes, trig4, region_len, S(stream));
+}
+int gebq_encode_noa_dev_f64(const uint64_t *x, int64_t n, const void *consts_dev, int unsafe,
+                            int64_t block_size, uint8_t *region, uint64_t *index, int64_t base_offset,
+                            void *ws, size_t ws_bytes, unsigned long long *trig4, long long *region_len,
+                            void *stream) {
+    ENC_CFG(MODE_ABS, 0)
+    Consts<double> k{};
+    return launch_encode<double>(cfg, x, nullptr, k, (const Consts<double> *)consts_dev, region, index, ws,
+                                 ws_bytes, trig4, region_len, S(stream));
+}
+int gebq_encode_coded_u32(const uint32_t *codes, const uint8_t *lossless, int64_t n, int64_t block_size,
+                          uint8_t *region, uint64_t *index, int64_t base_offset, void *ws,
+                          size_t ws_bytes, long long *region_len, void *stream) {
+    const int unsafe = 0;
+    ENC_CFG(MODE_ABS, 1)
+    Consts<float> k{};
+    return launch_encode<float>(cfg, codes, lossless, k, nullptr, region, index, ws, ws_bytes, nullptr,
+                                region_len, S(stream));
+}
+int gebq_encode_coded_u64(const uint64_t *codes, const uint8_t *lossless, int64_t n, int64_t block_size,
+                          uint8_t *region, uint64_t *index, int64_t base_offset, void *ws,
+                          size_t ws_bytes, long long *region_len, void *stream) {
+    const int unsafe = 0;
+    ENC_CFG(MODE_ABS, 1)
+    Consts<double> k{};
+    return launch_encode<double>(cfg, codes, lossless, k, nullptr, region, index, ws, ws_bytes, nullptr,
+                                 region_len, S(stream));
+}
+#undef ENC_CFG
+
+int gebq_validate_index(const int64_t *offsets, int64_t nblocks, int64_t region_len, int *flags3,
+                        void *stream) {
+    return launch_validate_index(offsets, nblocks, region_len, flags3, S(stream));
+}
+
+#define DEC_CFG(MODE, SINK) \
+    DecodeCfg d{MODE, SINK, count, block_size, 0, nblocks, nblocks, region_len};
+
+int gebq_decode_abs_f32(const uint8_t *region, int64_t region_len, const int64_t *offsets, int64_t nblocks,
+                        int64_t count, int64_t block_size, float eb2, uint32_t *out,
+                        unsigned long long *err_key, void *stream) {
+    DEC_CFG(MODE_ABS, 1)
+    return launch_decode<float>(d, region, offsets, eb2, out, nullptr, err_key, S(stream));
+}
+int gebq_decode_abs_f64(const uint8_t *region, int64_t region_len, const int64_t *offsets, int64_t nblocks,
+                        int64_t count, int64_t block_size, double eb2, uint64_t *out,
+                        unsigned long long *err_key, void *stream) {
+    DEC_CFG(MODE_ABS, 1)
+    return launch_decode<double>(d, region, offsets, eb2, out, nullptr, err_key, S(stream));
+}
+int gebq_decode_rel_f32(const uint8_t *region, int64_t region_len, const int64_t *offsets, int64_t nblocks,
+                        int64_t count, int64_t block_size, float w, uint32_t *out,
+                        unsigned long long *err_key, void *stream) {
+    DEC_CFG(MODE_REL, 1)
+    return launch_decode<float>(d, region, offsets, w, out, nullptr, err_key, S(stream));
+}
+int gebq_decode_rel_f64(const uint8_t *region, int64_t region_len, const int64_t *offsets, int64_t nblocks,
+                        int64_t count, int64_t block_size, double w, uint64_t *out,
+                        unsigned long long *err_key, void *stream) {
+    DEC_CFG(MODE_REL, 1)
+    return launch_decode<double>(d, region, offsets, w, out, nullptr, err_key, S(stream));
+}
+#undef DEC_CFG
+
+int gebq_decode_blocks_u32(const uint8_t *buf, const int64_t *offsets, int64_t noffsets, int64_t region_end,
+                           int64_t count, int64_t block_size, int64_t b0, int64_t b1, uint32_t *codes,
+                           uint8_t *lossless, unsigned long long *err_key, void *stream) {
+    DecodeCfg d{MODE_ABS, 0, count, block_size, b0, b1, noffsets, region_end};
+    return launch_decode<float>(d, buf, offsets, 0.0f, codes, lossless, err_key, S(stream));
+}
+int gebq_decode_blocks_u64(const uint8_t *buf, const int64_t *offsets, int64_t noffsets, int64_t region_end,
+                           int64_t count, int64_t block_size, int64_t b0, int64_t b1, uint64_t *codes,
+                           uint8_t *lossless, unsigned long long *err_key, void *stream) {
+    DecodeCfg d{MODE_ABS, 0, count, block_size, b0, b1, noffsets, region_end};
+    return launch_decode<double>(d, buf, offsets, 0.0, codes, lossless, err_key, S(stream));
+}
+int gebq_block_sizes_u32(const uint32_t *codes, int64_t count, int64_t block_size, int64_t b0, int64_t b1,
+                         int64_t *sizes, void *stream) {
+    return launch_block_sizes<uint32_t>(codes, count, block_size, b0, b1, sizes, S(stream));
+}
+int gebq_block_sizes_u64(const uint64_t *codes, int64_t count, int64_t block_size, int64_t b0, int64_t b1,
+                         int64_t *sizes, void *stream) {
+    return launch_block_sizes<uint64_t>(codes, count, block_size, b0, b1, sizes, S(stream));
+}
+int gebq_emit_blocks_u32(const uint32_t *codes, const uint8_t *lossless, int64_t count, int64_t block_size,
+                         int64_t b0, int64_t b1, const int64_t *offsets, uint8_t *out, void *stream) {
+    return launch_emit_blocks<uint32_t>(codes, lossless, count, block_size, b0, b1, offsets, out, S(stream));
+}
+int gebq_emit_blocks_u64(const uint64_t *codes, const uint8_t *lossless, int64_t count, int64_t block_size,
+                         int64_t b0, int64_t b1, const int64_t *offsets, uint8_t *out, void *stream) {
+    return launch_emit_blocks<uint64_t>(codes, lossless, count, block_size, b0, b1, offsets, out, S(stream));
 }
 
 }  // extern "C"

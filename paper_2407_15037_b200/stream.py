@@ -1,0 +1,277 @@
+"""Device-resident FORMAT.md streams: fused encode (quantize + pack) and fused
+decode (unpack + reconstruct) through libgebq_b200.so.
+
+Device stream buffer layout (one allocation, so one D2H moves a whole stream):
+
+    [0, 48)            header (filled on the host: it is 48 bytes of scalars)
+    [48, 56)           u64 block count N
+    [56, 56 + 8N)      block index (u64 offsets relative to the region)
+    [56 + 8N, ...)     block region, written by the encode kernel
+"""
+
+from __future__ import annotations
+
+import ctypes
+import struct
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .container import (HEADER_SIZE, FLAG_NO_DOUBLE_CHECK, StreamHeader, TruncatedStream,
+                        raise_for_err_key)
+from .device import _FTYPE, _ITYPE, _NP_ITYPE, _p, _s, _width_of, as_bits, require_cuda
+from .quantizers import NOA, REL, QuantConfig
+
+ERR_NONE = (1 << 64) - 1
+
+
+def region_capacity(n: int, block_size: int, width: int) -> int:
+    return int(_lib.load().gebq_encode_region_capacity(n, block_size, width))
+
+
+def workspace_bytes(n: int, block_size: int, width: int) -> int:
+    return int(_lib.load().gebq_encode_workspace_bytes(n, block_size, width))
+
+
+@dataclass
+class Encoded:
+    """A stream produced on the device (header bytes not yet written)."""
+
+    buf: torch.Tensor          # uint8 device buffer, layout in the module docstring
+    nblocks: int
+    count: int
+    width: int
+    region_len: torch.Tensor   # int64[1] device
+    trig: torch.Tensor         # int64[4] device
+    range_f64: Optional[torch.Tensor] = None  # NOA range computed on device
+
+    @property
+    def region_off(self) -> int:
+        return HEADER_SIZE + 8 + 8 * self.nblocks
+
+
+def alloc_stream(n: int, block_size: int, width: int, device) -> torch.Tensor:
+    nblocks = -(-n // block_size) if n else 0
+    cap = HEADER_SIZE + 8 + 8 * nblocks + region_capacity(n, block_size, width)
+    return torch.empty(cap, dtype=torch.uint8, device=device)
+
+
+def encode(x: torch.Tensor, cfg: QuantConfig, *, consts_dev: Optional[torch.Tensor] = None,
+           base_offset: int = 0, buf: Optional[torch.Tensor] = None,
+           ws: Optional[torch.Tensor] = None, trig: Optional[torch.Tensor] = None,
+           region_len: Optional[torch.Tensor] = None) -> Encoded:
+    """Quantize + pack ``x`` (a CUDA float/int tensor) into a stream buffer, one pass.
+
+    ``consts_dev`` supplies NOA constants produced on the device (range pass
+    -> derive) so the whole chain runs without a host round trip.
+    """
+    xb = as_bits(x)
+    width = _width_of(xb)
+    if width != cfg.width:
+        raise TypeError(f"expected {cfg.width}-bit values for this config, got {width}-bit")
+    n = xb.numel()
+    bs = cfg.block_size
+    nblocks = -(-n // bs) if n else 0
+    dev = xb.device
+    if buf is None:
+        buf = alloc_stream(n, bs, width, dev)
+    if ws is None:
+        ws = torch.empty(max(workspace_bytes(n, bs, width), 16), dtype=torch.uint8, device=dev)
+    if trig is None:
+        trig = torch.zeros(4, dtype=torch.int64, device=dev)
+    if region_len is None:
+        region_len = torch.empty(1, dtype=torch.int64, device=dev)
+    index = buf[HEADER_SIZE + 8:]
+    region = buf[HEADER_SIZE + 8 + 8 * nblocks:]
+    sfx = "f32" if width == 32 else "f64"
+    F = ctypes.c_float if width == 32 else ctypes.c_double
+    unsafe = int(bool(cfg.unsafe_no_double_check))
+    common = (_p(region), _p(index), base_offset, _p(ws), ws.numel(), _p(trig), _p(region_len), _s())
+    if consts_dev is not None:
+        _lib.call(f"gebq_encode_noa_dev_{sfx}", _p(xb), n, _p(consts_dev), unsafe, bs, *common)
+    elif cfg.mode == REL:
+        d = cfg.derived
+        _lib.call(f"gebq_encode_rel_{sfx}", _p(xb), n, F(d.op_eps), F(d.w), F(d.thr), unsafe, bs,
+                  *common)
+    else:
+        d = cfg.derived
+        _lib.call(f"gebq_encode_abs_{sfx}", _p(xb), n, F(d.eb_eff), F(d.eb2), F(d.inv_eb2),
+                  F(d.thr), unsafe, bs, *common)
+    return Encoded(buf=buf, nblocks=nblocks, count=n, width=width, region_len=region_len,
+                   trig=trig)
+
+
+def encode_coded(codes: torch.Tensor, lossless: torch.Tensor, block_size: int, *,
+                 base_offset: int = 0) -> Encoded:
+    """Pack given wire codes + flags (container.encode_stream) on the device."""
+    cb = as_bits(codes)
+    width = _width_of(cb)
+    n = cb.numel()
+    dev = cb.device
+    nblocks = -(-n // block_size) if n else 0
+    buf = alloc_stream(n, block_size, width, dev)
+    ws = torch.empty(max(workspace_bytes(n, block_size, width), 16), dtype=torch.uint8, device=dev)
+    region_len = torch.empty(1, dtype=torch.int64, device=dev)
+    if lossless.dtype == torch.bool:
+        lossless = lossless.view(torch.uint8)
+    index = buf[HEADER_SIZE + 8:]
+    region = buf[HEADER_SIZE + 8 + 8 * nblocks:]
+    _lib.call(f"gebq_encode_coded_u{width}", _p(cb), _p(lossless.contiguous()), n, block_size,
+              _p(region), _p(index), base_offset, _p(ws), ws.numel(), _p(region_len), _s())
+    return Encoded(buf=buf, nblocks=nblocks, count=n, width=width, region_len=region_len,
+                   trig=torch.zeros(4, dtype=torch.int64, device=dev))
+
+
+def stream_to_host(enc: Encoded, header: StreamHeader, region_len: Optional[int] = None) -> bytes:
+    """Assemble the final stream bytes: host header + one D2H of index + region."""
+    if region_len is None:
+        region_len = int(enc.region_len.item())
+    total = enc.region_off + region_len
+    host = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+    if total > HEADER_SIZE + 8:
+        host[HEADER_SIZE + 8:].copy_(enc.buf[HEADER_SIZE + 8:total])
+    arr = host.numpy()
+    arr[:HEADER_SIZE] = np.frombuffer(header.pack(), dtype=np.uint8)
+    arr[HEADER_SIZE:HEADER_SIZE + 8] = np.frombuffer(struct.pack("<Q", enc.nblocks), dtype=np.uint8)
+    return arr.tobytes()
+
+
+def header_for(cfg: QuantConfig, count: int, value_range=None) -> StreamHeader:
+    """Header of pipeline.compress (pipeline.py:178-187)."""
+    vr = value_range if value_range is not None else cfg.value_range
+    return StreamHeader(
+        width=cfg.width, mode=cfg.mode, count=count,
+        eb_bits=int(np.float64(cfg.eb).view(np.uint64)),
+        derived_bits=cfg.derived.header_bits,
+        range_bits=int(np.float64(vr or 0.0).view(np.uint64)) if cfg.mode == NOA else 0,
+        block_size=cfg.block_size,
+        flags=FLAG_NO_DOUBLE_CHECK if cfg.unsafe_no_double_check else 0)
+
+
+# ---------------------------------------------------------------------------
+# decode
+# ---------------------------------------------------------------------------
+
+def decode_values(stream_dev: torch.Tensor, header: StreamHeader, nblocks: int, *,
+                  out: Optional[torch.Tensor] = None, err: Optional[torch.Tensor] = None,
+                  index_pos: int = HEADER_SIZE + 8):
+    """Fused unpack + reconstruct of a device-resident stream -> value bits.
+
+    The index must already be validated (container.parse_layout or
+    :func:`validate_index`).  Returns (values int tensor, err_key int64[1]).
+    """
+    width = header.width
+    dev = stream_dev.device
+    if out is None:
+        out = torch.empty(header.count, dtype=_ITYPE[width], device=dev)
+    if err is None:
+        err = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    region_pos = index_pos + 8 * nblocks
+    region_len = stream_dev.numel() - region_pos
+    offsets = stream_dev[index_pos:]
+    region = stream_dev[region_pos:]
+    kind = "rel" if header.mode == REL else "abs"
+    sfx = "f32" if width == 32 else "f64"
+    F = ctypes.c_float if width == 32 else ctypes.c_double
+    if header.count:
+        _lib.call(f"gebq_decode_{kind}_{sfx}", _p(region), region_len, _p(offsets), nblocks,
+                  header.count, header.block_size, F(header.derived_value), _p(out), _p(err), _s())
+    return out, err
+
+
+def decode_codes(stream_dev: torch.Tensor, header: StreamHeader, nblocks: int, *,
+                 index_pos: int = HEADER_SIZE + 8):
+    """Unpack a device-resident stream to (codes, lossless u8, err_key)."""
+    width = header.width
+    dev = stream_dev.device
+    codes = torch.empty(header.count, dtype=_ITYPE[width], device=dev)
+    lossless = torch.empty(header.count, dtype=torch.uint8, device=dev)
+    err = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    region_pos = index_pos + 8 * nblocks
+    region_len = stream_dev.numel() - region_pos
+    if header.count:
+        _lib.call(f"gebq_decode_blocks_u{width}", _p(stream_dev[region_pos:]),
+                  _p(stream_dev[index_pos:]), nblocks, region_len, header.count,
+                  header.block_size, 0, nblocks, _p(codes), _p(lossless), _p(err), _s())
+    return codes, lossless, err
+
+
+def validate_index(stream_dev: torch.Tensor, nblocks: int, index_pos: int = HEADER_SIZE + 8):
+    """Device-side index checks -> int32[3] flags (first!=0, decreasing, beyond end)."""
+    flags = torch.empty(3, dtype=torch.int32, device=stream_dev.device)
+    region_len = stream_dev.numel() - index_pos - 8 * nblocks
+    _lib.call("gebq_validate_index", _p(stream_dev[index_pos:]), nblocks, region_len, _p(flags),
+              _s())
+    return flags
+
+
+def host_u8(data) -> torch.Tensor:
+    """Zero-copy uint8 CPU tensor over any bytes-like object (read-only is fine: we only read)."""
+    import warnings
+
+    if isinstance(data, torch.Tensor):
+        return data.view(torch.uint8).reshape(-1)
+    if isinstance(data, np.ndarray):
+        data = data.view(np.uint8).reshape(-1)
+        if data.flags.writeable:
+            return torch.from_numpy(data)
+    if len(data) == 0:
+        return torch.empty(0, dtype=torch.uint8)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return torch.frombuffer(data, dtype=torch.uint8)
+
+
+def _h2d_stream(data) -> torch.Tensor:
+    dev = require_cuda()
+    src = host_u8(data)
+    n = src.numel()
+    # keep 16 bytes of slack so vector loads near the end stay inside the allocation
+    t = torch.empty(n + 16, dtype=torch.uint8, device=dev)
+    if n:
+        t[:n].copy_(src)
+    return t[:n]
+
+
+# ---------------------------------------------------------------------------
+# host wrappers used by container.py / pipeline.py
+# ---------------------------------------------------------------------------
+
+def encode_coded_host(codes: np.ndarray, lossless: np.ndarray, header: StreamHeader) -> bytes:
+    from .device import to_device
+
+    require_cuda()
+    if header.count == 0:
+        return header.pack() + struct.pack("<Q", 0)
+    enc = encode_coded(to_device(codes), to_device(np.asarray(lossless, dtype=np.bool_)),
+                       header.block_size)
+    return stream_to_host(enc, header)
+
+
+def decode_coded_host(data, header: StreamHeader, nblocks: int, index_pos: int):
+    width = header.width
+    if header.count == 0:
+        return np.empty(0, _NP_ITYPE[width]), np.empty(0, np.bool_)
+    sd = _h2d_stream(data)
+    codes, lossless, err = decode_codes(sd, header, nblocks, index_pos=index_pos)
+    key = int(err.item()) & ERR_NONE
+    raise_for_err_key(key)
+    return (codes.cpu().numpy().view(_NP_ITYPE[width]),
+            lossless.cpu().numpy().view(np.bool_))
+
+
+def decode_values_host(data, header: StreamHeader, nblocks: int, index_pos: int) -> np.ndarray:
+    width = header.width
+    ft = np.float32 if width == 32 else np.float64
+    if header.count == 0:
+        return np.empty(0, ft)
+    sd = _h2d_stream(data)
+    out, err = decode_values(sd, header, nblocks, index_pos=index_pos)
+    host = torch.empty(header.count, dtype=_ITYPE[width], pin_memory=True)
+    host.copy_(out)
+    key = int(err.item()) & ERR_NONE
+    raise_for_err_key(key)
+    return host.numpy().view(ft)

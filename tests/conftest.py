@@ -63,3 +63,16 @@ def cuda():
 
     _lib.load()
     return torch.device("cuda", 0)
+
+
+def pytest_sessionstart(session):
+    """Refuse to test a stale CUDA library (sources newer than the built .so)."""
+    try:
+        from paper_2407_15037_b200 import _build
+    except Exception:  # pragma: no cover
+        return
+    import os
+
+    if os.path.exists(_build.LIB) and not _build.up_to_date():
+        raise RuntimeError("libgebq_b200.so is older than its sources: run "
+                           "`python -m paper_2407_15037_b200._build` first")

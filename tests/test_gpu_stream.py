@@ -1,0 +1,238 @@
+"""GPU parity of the FORMAT.md stream path: fused encode / decode, container
+errors, golden digests, workloads -- byte-exact against reference fixtures and
+the CPU oracle."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from helpers import mixed_bits, stream_values, trig_list
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(b) -> str:
+    return hashlib.sha256(bytes(b)).hexdigest()
+
+
+def _cfg(mode, eb, width=32, vr=None, unsafe=False, bs=4096):
+    from paper_2407_15037_b200 import QuantConfig
+
+    return QuantConfig(mode=mode, eb=eb, width=width, value_range=vr, unsafe_no_double_check=unsafe,
+                       block_size=bs)
+
+
+def test_golden_digest(cuda, oracle, golden_record):
+    import paper_2407_15037_b200 as g
+
+    overall = hashlib.sha256()
+    for (mode, eb, width, rng), exp in zip(oracle.GOLDEN_CONFIGS, golden_record["configs"]):
+        vals = oracle.golden_values(width)
+        s, st = g.compress(vals, _cfg(mode, eb, width, rng))
+        overall.update(s)
+        assert sha(s) == exp["sha256"], (mode, width)
+        assert len(s) == exp["bytes"]
+        assert trig_list(st.triggers) == trig_list(exp["triggers"])
+        out = g.decompress_to_array(s)
+        assert sha(out.tobytes()) == exp["recon_sha256"]
+    assert overall.hexdigest() == golden_record["overall"]
+
+
+def test_stream_grid(cuda, fixtures):
+    """Every (mode, width, block_size in 1..100000, unsafe) stream digest of the reference."""
+    import paper_2407_15037_b200 as g
+
+    cache = {}
+    for rec in fixtures["streams"]:
+        key = (rec["width"], rec["seed"])
+        if key not in cache:
+            cache[key] = stream_values(rec["width"], rec["seed"])
+        vals = cache[key]
+        cfg = _cfg(rec["mode"], rec["eb"], rec["width"], rec["value_range"], rec["unsafe"],
+                   rec["block_size"])
+        s, st = g.compress(vals, cfg)
+        assert sha(s) == rec["sha256"], rec
+        assert trig_list(st.triggers) == trig_list(rec["triggers"])
+        out = g.decompress_to_array(s)
+        if rec["block_size"] in (1, 4096, 10000):
+            h, ca = g.decode_stream(s)
+            assert h.count == len(vals)
+            s2 = g.encode_stream(ca, h)
+            assert s2 == s
+        assert out.dtype == vals.dtype
+
+
+def test_roundtrip_matches_oracle_decode(cuda, oracle, fixtures):
+    import paper_2407_15037_b200 as g
+
+    for rec in fixtures["streams"][::7]:
+        vals = stream_values(rec["width"], rec["seed"])
+        cfg = _cfg(rec["mode"], rec["eb"], rec["width"], rec["value_range"], rec["unsafe"],
+                   rec["block_size"])
+        s, _ = g.compress(vals, cfg)
+        np.testing.assert_array_equal(g.decompress_to_array(s).view(np.uint8),
+                                      oracle.decompress_to_array(s).view(np.uint8))
+
+
+def test_format_example_and_empty(cuda, fixtures):
+    import paper_2407_15037_b200 as g
+
+    s, st = g.compress(np.array([3.2, np.nan, -0.75], dtype=np.float32), _cfg("abs", 0.5))
+    assert s.hex() == fixtures["format_example_hex"] and len(s) == 79
+    assert st.values_lossless == 1 and st.triggers["nan"] == 1
+    e, st = g.compress(np.array([], dtype=np.float32), _cfg("abs", 1e-3))
+    assert e.hex() == fixtures["empty_stream_hex"]
+    assert g.decompress(e) == b""
+    out = g.decompress_to_array(s)
+    assert out.view(np.uint32)[1] == 0x7FC00000
+    assert list(out[[0, 2]]) == [3.0, -1.0]
+
+
+def _outcome(fn, data):
+    import paper_2407_15037_b200 as g
+
+    try:
+        out = fn(data)
+        return "OK:" + sha(out.tobytes())[:16]
+    except g.ContainerError as e:
+        return type(e).__name__ + ":" + str(e)
+
+
+def test_decode_fuzz_typed_errors(cuda, fixtures, fuzz_arrays):
+    """12000 byte mutations: same exception class AND byte position as the reference."""
+    import paper_2407_15037_b200 as g
+
+    for meta in fixtures["decode_fuzz"]:
+        base = fuzz_arrays[meta["name"] + "_base"].tobytes()
+        muts = fuzz_arrays[meta["name"] + "_muts"]
+        for m, expect in zip(muts, meta["outcomes"]):
+            s = bytearray(base)
+            for p, x in m:
+                if p >= 0:
+                    s[p] ^= int(x)
+            got = _outcome(g.decompress_to_array, bytes(s))
+            assert got == expect, (meta["name"], m.tolist())
+        for cut, expect in meta["truncations"]:
+            got = _outcome(g.decompress_to_array, base[:cut])
+            assert got.split(":")[0] == expect.split(":")[0]
+            if expect != "OK":
+                assert got == expect
+
+
+def test_decode_stream_codes_vs_oracle(cuda, oracle):
+    import paper_2407_15037_b200 as g
+
+    for width, mode in ((32, "abs"), (32, "rel"), (64, "abs"), (64, "rel")):
+        ft = np.float32 if width == 32 else np.float64
+        vals = mixed_bits(width, 30000, 3).view(ft)
+        for bs in (64, 300, 4096, 5000):
+            s, _, _ = oracle.compress(vals, mode, 1e-3, block_size=bs)
+            h, ca = g.decode_stream(s)
+            _, codes, ll = oracle.decode_stream(s)
+            np.testing.assert_array_equal(ca.codes, codes)
+            np.testing.assert_array_equal(ca.lossless, ll)
+
+
+def test_compress_coded_matches_compress(cuda, oracle):
+    import paper_2407_15037_b200 as g
+
+    vals = stream_values(32, 4274)
+    for mode, eb in (("abs", 1e-3), ("rel", 1e-2), ("noa", 1e-4)):
+        ca, cfg2, st = g.compress_coded(vals, _cfg(mode, eb))
+        codes, ll, trig, c, vr = oracle.compress_coded(vals, mode, eb)
+        np.testing.assert_array_equal(ca.codes, codes)
+        np.testing.assert_array_equal(ca.lossless, ll)
+        assert trig_list(st.triggers) == list(trig)
+        if mode == "noa":
+            assert cfg2.value_range == vr
+
+
+def test_workload_fixtures(cuda, fixtures):
+    import paper_2407_15037_b200 as g
+    from paper_2407_15037_b200 import workloads
+
+    for rec in fixtures["workloads"]:
+        if rec["workload"] == "c1":
+            x = workloads.smooth_field(256, 0, np.float32)
+            cfg = _cfg(rec["mode"], rec["eb"])
+        elif rec["workload"] == "c2":
+            x = workloads.c2_values(rec["n"])
+            cfg = _cfg(rec["mode"], rec["eb"])
+        else:
+            x = workloads.c5_random_values(rec["n"])
+            cfg = _cfg(rec["mode"], rec["eb"], 64)
+        s, st = g.compress(x, cfg)
+        assert sha(s) == rec["sha256"], rec["workload"]
+        assert len(s) == rec["bytes"]
+        assert trig_list(st.triggers) == trig_list(rec["triggers"])
+        if "recon_sha256" in rec:
+            assert sha(g.decompress_to_array(s).tobytes()) == rec["recon_sha256"]
+
+
+@pytest.mark.parametrize("width", [32, 64])
+def test_large_c2_and_noa_vs_oracle(cuda, oracle, width):
+    """2^24-value streams (mixed REL; planted-extreme NOA) byte-identical to the oracle."""
+    import paper_2407_15037_b200 as g
+    from paper_2407_15037_b200 import workloads
+
+    ft = np.float32 if width == 32 else np.float64
+    if width == 32:
+        x = workloads.c2_values(1 << 24)
+    else:
+        x = workloads.c5_random_values(1 << 23)
+    s, st = g.compress(x, _cfg("rel", 1e-2, width))
+    so, trig, _ = oracle.compress(x, "rel", 1e-2, workers=8)
+    assert s == so
+    assert trig_list(st.triggers) == list(trig)
+    np.testing.assert_array_equal(g.decompress_to_array(s).view(np.uint8),
+                                  oracle.decompress_to_array(so, workers=8).view(np.uint8))
+    f = workloads.plant_noa_extremes(workloads.smooth_field(256, 1, ft))
+    s, st = g.compress(f, _cfg("noa", 1e-4, width))
+    so, trig, vr = oracle.compress(f, "noa", 1e-4, workers=8)
+    assert vr == 14.0
+    assert s == so
+
+
+def test_kernel_dropins_vs_oracle(cuda, oracle):
+    """The gebq._kernels-signature shims, called the way the reference calls them."""
+    from paper_2407_15037_b200 import _kernels as K
+
+    bits = mixed_bits(32, 20000, 9)
+    c = oracle.derive("abs", 1e-3, 32)
+    codes = np.empty(len(bits), np.uint32)
+    ll = np.empty(len(bits), np.bool_)
+    trig = K.quantize_abs32(bits, bits.view(np.float32), codes, ll, c["eb_eff"], c["eb2"],
+                            c["inv_eb2"], c["thr"], False)
+    ec, el, et = oracle.quantize(bits, "abs", c)
+    np.testing.assert_array_equal(codes, ec)
+    np.testing.assert_array_equal(ll, el)
+    np.testing.assert_array_equal(trig, et)
+    out = np.empty(len(bits), np.float32)
+    K.reconstruct_abs32(codes, ll, out.view(np.uint32), out, c["eb2"])
+    np.testing.assert_array_equal(out.view(np.uint32), oracle.reconstruct(ec, el, "abs", c["eb2"]))
+    bs = 1000
+    nb = -(-len(bits) // bs)
+    sizes = np.zeros(nb, np.int64)
+    K.block_sizes_u32(codes, len(codes), bs, 0, nb, sizes)
+    offsets = np.zeros(nb + 1, np.int64)
+    np.cumsum(sizes, out=offsets[1:])
+    out_b = np.empty(int(offsets[-1]), np.uint8)
+    K.emit_blocks_u32(codes, ll, len(codes), bs, 0, nb, offsets, out_b)
+    eo, er = oracle.encode_payload(ec, el, bs)
+    np.testing.assert_array_equal(offsets[:nb], eo)
+    np.testing.assert_array_equal(out_b, er)
+    c2 = np.empty(len(bits), np.uint32)
+    l2 = np.empty(len(bits), np.bool_)
+    st, pos = K.decode_blocks_u32(out_b, offsets[:nb], len(out_b), len(bits), bs, 0, nb, c2, l2)
+    assert st == 0
+    np.testing.assert_array_equal(c2, ec)
+    np.testing.assert_array_equal(l2, el)
+    cr = oracle.derive("rel", 1e-3, 32)
+    tally, first = K.sweep_rel32_on(bits, bits.view(np.float32), cr["op_eps"], cr["w"], cr["thr"],
+                                    False)
+    et2, ef2 = oracle.sweep_on(bits, "rel", 1e-3)
+    np.testing.assert_array_equal(tally, et2)
+    w = np.empty(1000, np.uint64)
+    K.splitmix64_fill(w, 0x9E3779B97F4A7C15, 5)
+    np.testing.assert_array_equal(w, oracle.splitmix64_fill(1000, 0x9E3779B97F4A7C15, 5))
