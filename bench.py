@@ -1,0 +1,457 @@
+#!/usr/bin/env python
+"""bench.py -- B200 quantize/dequantize throughput for the gebq hot path.
+
+One *step* = one pass of the hot path over one batch: fused encode
+(quantize + FORMAT.md pack, one kernel) then fused decode (unpack +
+reconstruct, one kernel) of the batch, data resident in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+Default workload = BASELINE.json configs[1] (C2): REL f32 eb=1e-2, 2^26
+mixed values per GPU (NaN/Inf/denormal/huge outliers), weak scaling, no
+data-path collective.  ``--workload c3`` runs NOA (range pass -> NCCL MAX
+allreduce of the two order keys -> derive -> encode -> decode), strong
+scaling over a 2^30-value field.
+
+Metric basis: GB/s of uncompressed values through quantize + dequantize,
+i.e. (n*W encoded + n*W decoded) / step time, summed over ranks (the
+paper's input-bytes convention applied to both stages).  Rank 0 prints ONE
+JSON line.  ``--impl reference`` times the reference algorithm on the host
+cores instead (the plain-C oracle port, oracle/, all threads), same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "quantize/dequantize GB/s at 1/2/4/8 B200 vs HBM roofline; 0 bound violations"
+
+WORKLOADS = {
+    "c2": dict(desc="C2: REL f32 eb=1e-2, mixed NaN/Inf/denormal/huge (SURVEY App. C), 2^26 values per GPU",
+               mode="rel", eb=1e-2, width=32, n=1 << 26, scaling="weak"),
+    "c1": dict(desc="C1: ABS f32 eb=1e-3, 256^3 smooth field per GPU", mode="abs", eb=1e-3,
+               width=32, n=1 << 24, scaling="weak"),
+    "c3": dict(desc="C3: NOA f32 eb=1e-4, 1024^3 smooth field (2^30 values) sharded over the GPUs",
+               mode="noa", eb=1e-4, width=32, n=1 << 30, scaling="strong"),
+    "c5": dict(desc="C5: ABS f64 eb=1e-3, 2^28 random splitmix64 doubles per GPU", mode="abs",
+               eb=1e-3, width=64, n=1 << 28, scaling="weak"),
+    "c5rel": dict(desc="C5: REL f64 eb=1e-3, 2^28 random splitmix64 doubles per GPU", mode="rel",
+                  eb=1e-3, width=64, n=1 << 28, scaling="weak"),
+}
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    return ap.parse_args()
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(workload: str):
+    """ncu dram bytes per launch for the dominant kernel, if a capture was committed."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(workload)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML, same counters as the nvidia-smi line)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int, period_s: float = 0.002):
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._th = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+        self.period = period_s
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._th = threading.Thread(target=self._run, daemon=True)
+            self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._th is not None:
+            self._th.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------
+# inputs
+# ---------------------------------------------------------------------------
+def make_input(wl: dict, name: str, rank: int, world: int, device):
+    """Per-rank shard on the device (contiguous, block-aligned part of a global array)."""
+    import torch
+
+    from paper_2407_15037_b200 import device as gdev
+    from paper_2407_15037_b200 import workloads
+
+    if wl["scaling"] == "strong":
+        n_total = wl["n"]
+        n = n_total // world
+    else:
+        n = wl["n"]
+    start = rank * n
+    if name == "c2":
+        return gdev.mixed_f32(n, workloads.C2_SEED, start, device=device), n
+    if name in ("c5", "c5rel"):
+        return gdev.splitmix64(n, workloads.C5_SEED, start, device=device), n
+    if name == "c1":
+        x = workloads.smooth_field(256, rank, np.float32)
+        return torch.from_numpy(x.view(np.int32)).to(device), n
+    if name == "c3":
+        # 1024^3 smooth field in f64 math, cast once; noise from the CUDA Philox
+        # generator (seed 1) -- both GPU and CPU checkers consume these same bits.
+        side = 1024
+        g = torch.Generator(device=device)
+        g.manual_seed(1 + rank)
+        idx = torch.arange(start, start + n, device=device, dtype=torch.int64)
+        i = (idx // (side * side)).double()
+        j = ((idx // side) % side).double()
+        k = (idx % side).double()
+        two_pi = 2 * np.pi
+        x = (5.0 * torch.sin(two_pi * i / side) * torch.cos(two_pi * j / side)
+             * torch.sin(two_pi * k / (side // 2)))
+        x = x + 0.02 * torch.randn(n, generator=g, device=device, dtype=torch.float64)
+        x = x.float()
+        if rank == 0:
+            x[0] = float("nan")
+            x[1] = float("inf")
+            x[2] = -7.0
+        if rank == world - 1:
+            x[-1] = 7.0
+        del i, j, k, idx
+        return x.view(torch.int32), n
+    raise ValueError(name)
+
+
+# ---------------------------------------------------------------------------
+# reference arm / CPU baseline: the oracle port on the host cores
+# ---------------------------------------------------------------------------
+def host_input(name: str, wl: dict, n: int) -> np.ndarray:
+    from paper_2407_15037_b200 import workloads
+
+    if name == "c2":
+        return workloads.c2_values(n)
+    if name in ("c5", "c5rel"):
+        return workloads.c5_random_values(n)
+    if name == "c1":
+        return workloads.smooth_field(256, 0, np.float32)
+    if name == "c3":
+        return workloads.plant_noa_extremes(workloads.smooth_field(1024, 1, np.float32))[:n]
+    raise ValueError(name)
+
+
+def cpu_roundtrip_gbs(x: np.ndarray, wl: dict, workers: int, reps: int):
+    """Median GB/s (same basis) of oracle compress + decompress on the host cores."""
+    from oracle import oracle as orc
+
+    orc.lib()
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        s, _, _ = orc.compress(x, wl["mode"], wl["eb"], workers=workers)
+        y = orc.decompress_to_array(s, workers=workers)
+        times.append(time.perf_counter() - t0)
+        del s, y
+    t = float(np.median(times))
+    return 2 * x.nbytes / t / 1e9, t, times
+
+
+def run_reference(args, wl, name):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    n = wl["n"] if wl["scaling"] == "weak" else wl["n"]
+    cores = os.cpu_count() or 1
+    x = host_input(name, wl, n)
+    from oracle import oracle as orc
+
+    orc.lib()
+    for _ in range(max(args.warmup, 1)):
+        s, _, _ = orc.compress(x, wl["mode"], wl["eb"], workers=cores)
+        orc.decompress_to_array(s, workers=cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        s, _, _ = orc.compress(x, wl["mode"], wl["eb"], workers=cores)
+        orc.decompress_to_array(s, workers=cores)
+        times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    value = 2 * x.nbytes / t / 1e9
+    sample = f"full {name} batch ({n} values, {x.nbytes} B) per step, compress + decompress"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None,
+        "dtype": "f32" if wl["width"] == 32 else "f64", "data": "synthetic",
+        "config": {"workload": wl["desc"], "n": n, "block_size": 4096,
+                   "gbs_basis": "uncompressed bytes encoded + decoded per second"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "reference algorithm = plain-C restatement of gebq's numba loops (oracle/, pinned "
+                "to the reference's golden digests); the Python reference does not ship to the GPU box",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def main():
+    args = parse_args()
+    args.warmup = max(args.warmup, 3)
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, wl, args.workload)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_15037_b200 import _lib, device as gdev, stream
+    from paper_2407_15037_b200.container import StreamHeader
+    from paper_2407_15037_b200.pipeline import compress, decompress_to_array
+    from paper_2407_15037_b200.quantizers import NOA, QuantConfig
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.load()
+
+    x, n = make_input(wl, args.workload, rank, world, dev)
+    W = wl["width"] // 8
+    cfg = QuantConfig(mode=wl["mode"], eb=wl["eb"], width=wl["width"])
+    bs = cfg.block_size
+    nblocks = -(-n // bs)
+    buf = stream.alloc_stream(n, bs, wl["width"], dev)
+    ws = torch.empty(max(stream.workspace_bytes(n, bs, wl["width"]), 16), dtype=torch.uint8, device=dev)
+    trig = torch.zeros(4, dtype=torch.int64, device=dev)
+    rlen = torch.empty(1, dtype=torch.int64, device=dev)
+    out = torch.empty(n, dtype=x.dtype, device=dev)
+    err = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    keys = torch.empty(2, dtype=torch.int64, device=dev)
+    # decode header: NOA reconstructs with the ABS kernel and takes eb2 from the device
+    hdr = StreamHeader(width=wl["width"], mode="abs" if wl["mode"] == NOA else wl["mode"],
+                       count=n, eb_bits=0, derived_bits=cfg.derived.header_bits if wl["mode"] != NOA else 0,
+                       block_size=bs)
+    st = torch.cuda.current_stream()
+
+    def step(ev=None):
+        consts = None
+        if wl["mode"] == NOA:
+            gdev.noa_keys(x, keys)
+            if world > 1:
+                dist.all_reduce(keys, op=dist.ReduceOp.MAX)  # the one data-path collective
+            consts, _ = gdev.noa_derive(keys, wl["eb"], wl["width"])
+        if ev is not None:
+            ev[0].record(st)
+        trig.zero_()
+        enc = stream.encode(x, cfg, consts_dev=consts, buf=buf, ws=ws, trig=trig, region_len=rlen)
+        if ev is not None:
+            ev[1].record(st)
+        err.fill_(-1)
+        stream.decode_values(buf, hdr, nblocks, out=out, err=err, region_len_dev=rlen,
+                             derived_dev=None if consts is None else consts[1:])
+        if ev is not None:
+            ev[2].record(st)
+        return enc
+
+    # warm-up + one correctness probe: decoded stream must be error-free and,
+    # for lossless values, the trigger counts must add up
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stream_bytes = int(rlen.item()) + 56 + 8 * nblocks
+    assert int(err.item()) == -1, "decode reported an error on a freshly encoded stream"
+    trig_h = trig.cpu().numpy().tolist()
+
+    # timed region: K device steps, events on the launching stream
+    events = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        t_start.record(st)
+        for i in range(args.steps):
+            step(events[i])
+        t_end.record(st)
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    enc_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in events]))
+    dec_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in events]))
+    t = torch.tensor([total_ms, enc_ms, dec_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, enc_ms, dec_ms = t.tolist()
+    ms_per_step = total_ms / args.steps
+    n_all = n * world
+    value = 2 * n_all * W / (ms_per_step * 1e-3) / 1e9
+
+    peak, peak_kind = load_peaks()
+    enc_bytes = n * W + stream_bytes            # algorithmic: read values, write stream
+    dec_bytes = stream_bytes + n * W            # read stream, write values
+    enc_gbs = enc_bytes / (enc_ms * 1e-3) / 1e9
+    dec_gbs = dec_bytes / (dec_ms * 1e-3) / 1e9
+    dominant = ("encode", enc_ms, enc_bytes, enc_gbs) if enc_ms >= dec_ms else ("decode", dec_ms, dec_bytes, dec_gbs)
+    traffic = load_traffic(args.workload)
+
+    # end-to-end through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        ft = np.float32 if wl["width"] == 32 else np.float64
+        pinned = torch.empty(n, dtype=x.dtype, pin_memory=True)
+        pinned.copy_(x)
+        xh = pinned.numpy().view(ft)
+        e2e_cfg = QuantConfig(mode=wl["mode"], eb=wl["eb"], width=wl["width"])
+        for _ in range(2):
+            s, _ = compress(xh, e2e_cfg)
+            decompress_to_array(s)
+        k2 = args.e2e_steps or max(3, min(args.steps, 10))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        h2d = d2h = 0
+        for _ in range(k2):
+            s, st_ = compress(xh, e2e_cfg)
+            y = decompress_to_array(s)
+            h2d += xh.nbytes + len(s)
+            d2h += len(s) + y.nbytes
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+        tt = torch.tensor([el], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        el = tt.item()
+        e2e = {"value": 2 * n_all * W / (el / k2) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": int(h2d / k2), "d2h_bytes_per_step": int(d2h / k2),
+               "steps": k2, "ms_per_step": el / k2 * 1e3,
+               "api": "paper_2407_15037_b200.compress + decompress_to_array (pinned numpy in, bytes/ndarray out)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        xh_cpu = host_input(args.workload, wl, n)
+        gbs, tmed, times = cpu_roundtrip_gbs(xh_cpu, wl, cores, reps=5)
+        cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port",
+               "sample": f"full {args.workload} batch ({n} values) compress+decompress, median of 5 "
+                         f"({tmed * 1e3:.0f} ms each) on {cores} threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": wl["scaling"], "vs_baseline": None,
+            "dtype": "f32" if wl["width"] == 32 else "f64", "data": "synthetic",
+            "config": {"workload": wl["desc"], "n_per_gpu": n, "block_size": bs,
+                       "parallelism": f"dp{world} (contiguous block-aligned shards)",
+                       "l2": "inputs larger than L2 (values %d MiB, stream %d MiB per GPU)" % (
+                           n * W >> 20, stream_bytes >> 20),
+                       "gbs_basis": "uncompressed bytes encoded + decoded per second, all GPUs"},
+            "e2e": e2e,
+            "roofline": {"bound": "hbm", "kernel": dominant[0], "achieved": dominant[3],
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": dominant[3] / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": dominant[2],
+                         "ms_per_launch": dominant[1]},
+            "kernels": {"encode": {"ms": enc_ms, "gbs": enc_gbs, "frac": enc_gbs / peak,
+                                   "bytes": enc_bytes, "input_gbs": n * W / (enc_ms * 1e-3) / 1e9},
+                        "decode": {"ms": dec_ms, "gbs": dec_gbs, "frac": dec_gbs / peak,
+                                   "bytes": dec_bytes, "input_gbs": n * W / (dec_ms * 1e-3) / 1e9}},
+            "stream_bytes_per_value": stream_bytes / n, "triggers": trig_h,
+            "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -45,6 +45,8 @@ int gebq_b200_abi_version(void);
 const char *gebq_b200_last_error(void);
 /* SM count of the current device (a cheap probe that the CUDA backend works). */
 int gebq_b200_sm_count(void);
+/* Number of kernels this library has launched in the process (for audits). */
+unsigned long long gebq_b200_launch_count(void);
 
 /* ---- quantize: quantize_{abs,rel}{32,64} (_kernels.py:86-285) ------------
  * x -> (codes, lossless); trig4 += {nan, inf, guard, double_check} counts
@@ -186,7 +188,10 @@ int gebq_encode_coded_u64(const uint64_t *codes, const uint8_t *lossless, int64_
  * validate_index: the index checks of decode_stream (container.py:283-291);
  *   flags3 = {first offset != 0, offsets decreasing, last offset > region_len}.
  * decode_{abs,rel}_*: unpack + reconstruct fused (decode_blocks_* then
- *   reconstruct_*, pipeline.py:195-213) straight to value bits.
+ *   reconstruct_*, pipeline.py:195-213) straight to value bits.  Optional
+ *   device-side inputs (NULL = use the scalar): region_len_dev (the encoder's
+ *   *region_len, so decode can follow encode without a host round trip) and
+ *   derived_dev (eb2 / w written by gebq_noa_derive_*: consts + 1 element).
  * decode_blocks_u{32,64}: decode_blocks_* (_kernels.py:642-664) to codes +
  *   lossless flags for blocks [b0, b1).
  * Errors: *err_key (device, caller sets UINT64_MAX) is atomically MIN-ed with
@@ -196,17 +201,21 @@ int gebq_encode_coded_u64(const uint64_t *codes, const uint8_t *lossless, int64_
  *   (container.py:308-311).                                                  */
 int gebq_validate_index(const int64_t *offsets, int64_t nblocks, int64_t region_len,
                         int *flags3, void *stream);
-int gebq_decode_abs_f32(const uint8_t *region, int64_t region_len, const int64_t *offsets,
-                        int64_t nblocks, int64_t count, int64_t block_size, float eb2,
+int gebq_decode_abs_f32(const uint8_t *region, int64_t region_len,
+                        const long long *region_len_dev, const int64_t *offsets, int64_t nblocks,
+                        int64_t count, int64_t block_size, float eb2, const void *derived_dev,
                         uint32_t *out, unsigned long long *err_key, void *stream);
-int gebq_decode_abs_f64(const uint8_t *region, int64_t region_len, const int64_t *offsets,
-                        int64_t nblocks, int64_t count, int64_t block_size, double eb2,
+int gebq_decode_abs_f64(const uint8_t *region, int64_t region_len,
+                        const long long *region_len_dev, const int64_t *offsets, int64_t nblocks,
+                        int64_t count, int64_t block_size, double eb2, const void *derived_dev,
                         uint64_t *out, unsigned long long *err_key, void *stream);
-int gebq_decode_rel_f32(const uint8_t *region, int64_t region_len, const int64_t *offsets,
-                        int64_t nblocks, int64_t count, int64_t block_size, float w,
+int gebq_decode_rel_f32(const uint8_t *region, int64_t region_len,
+                        const long long *region_len_dev, const int64_t *offsets, int64_t nblocks,
+                        int64_t count, int64_t block_size, float w, const void *derived_dev,
                         uint32_t *out, unsigned long long *err_key, void *stream);
-int gebq_decode_rel_f64(const uint8_t *region, int64_t region_len, const int64_t *offsets,
-                        int64_t nblocks, int64_t count, int64_t block_size, double w,
+int gebq_decode_rel_f64(const uint8_t *region, int64_t region_len,
+                        const long long *region_len_dev, const int64_t *offsets, int64_t nblocks,
+                        int64_t count, int64_t block_size, double w, const void *derived_dev,
                         uint64_t *out, unsigned long long *err_key, void *stream);
 int gebq_decode_blocks_u32(const uint8_t *buf, const int64_t *offsets, int64_t noffsets,
                            int64_t region_end, int64_t count, int64_t block_size, int64_t b0,

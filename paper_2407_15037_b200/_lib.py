@@ -30,6 +30,7 @@ SIGNATURES = {
     "gebq_b200_abi_version": [],
     "gebq_b200_last_error": [],
     "gebq_b200_sm_count": [],
+    "gebq_b200_launch_count": [],
     "gebq_quantize_abs_f32": [_vp, _vp, _vp, _i64, _f32, _f32, _f32, _f32, _int, _vp, _vp],
     "gebq_quantize_abs_f64": [_vp, _vp, _vp, _i64, _f64, _f64, _f64, _f64, _int, _vp, _vp],
     "gebq_quantize_rel_f32": [_vp, _vp, _vp, _i64, _f32, _f32, _f32, _int, _vp, _vp],
@@ -67,10 +68,10 @@ SIGNATURES = {
     "gebq_encode_coded_u32": [_vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp, ctypes.c_size_t, _vp, _vp],
     "gebq_encode_coded_u64": [_vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp, ctypes.c_size_t, _vp, _vp],
     "gebq_validate_index": [_vp, _i64, _i64, _vp, _vp],
-    "gebq_decode_abs_f32": [_vp, _i64, _vp, _i64, _i64, _i64, _f32, _vp, _vp, _vp],
-    "gebq_decode_abs_f64": [_vp, _i64, _vp, _i64, _i64, _i64, _f64, _vp, _vp, _vp],
-    "gebq_decode_rel_f32": [_vp, _i64, _vp, _i64, _i64, _i64, _f32, _vp, _vp, _vp],
-    "gebq_decode_rel_f64": [_vp, _i64, _vp, _i64, _i64, _i64, _f64, _vp, _vp, _vp],
+    "gebq_decode_abs_f32": [_vp, _i64, _vp, _vp, _i64, _i64, _i64, _f32, _vp, _vp, _vp, _vp],
+    "gebq_decode_abs_f64": [_vp, _i64, _vp, _vp, _i64, _i64, _i64, _f64, _vp, _vp, _vp, _vp],
+    "gebq_decode_rel_f32": [_vp, _i64, _vp, _vp, _i64, _i64, _i64, _f32, _vp, _vp, _vp, _vp],
+    "gebq_decode_rel_f64": [_vp, _i64, _vp, _vp, _i64, _i64, _i64, _f64, _vp, _vp, _vp, _vp],
     "gebq_decode_blocks_u32": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp],
     "gebq_decode_blocks_u64": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp],
     "gebq_block_sizes_u32": [_vp, _i64, _i64, _i64, _i64, _vp, _vp],
@@ -78,7 +79,7 @@ SIGNATURES = {
     "gebq_emit_blocks_u32": [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp],
     "gebq_emit_blocks_u64": [_vp, _vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp],
 }
-_RESTYPES = {"gebq_b200_last_error": ctypes.c_char_p, "gebq_encode_region_capacity": _i64,
+_RESTYPES = {"gebq_b200_last_error": ctypes.c_char_p, "gebq_b200_launch_count": ctypes.c_ulonglong, "gebq_encode_region_capacity": _i64,
              "gebq_encode_workspace_bytes": ctypes.c_size_t}
 
 _lock = threading.Lock()
@@ -119,3 +120,8 @@ def call(name: str, *args) -> int:
 
 def exported_symbols() -> list[str]:
     return list(SIGNATURES)
+
+
+def launch_count() -> int:
+    """Kernels launched by libgebq_b200.so so far in this process."""
+    return int(load().gebq_b200_launch_count())

@@ -2,6 +2,7 @@
 // Thin: argument plumbing + error text; all work is in the kernel files.
 #include <cstdio>
 #include <cstring>
+#include <atomic>
 #include <string>
 
 #include "../../include/gebq_b200.h"
@@ -12,6 +13,9 @@
 namespace gebq {
 
 static thread_local std::string g_err;
+static std::atomic<unsigned long long> g_launches{0};
+
+void note_launch(int k) { g_launches.fetch_add((unsigned long long)k, std::memory_order_relaxed); }
 
 int set_error(cudaError_t e, const char *what) {
     g_err = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
@@ -24,6 +28,7 @@ int set_error_msg(int code, const char *msg) {
 int check_launch(const char *what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_error(e, what);
+    note_launch(1);
     return 0;
 }
 
@@ -52,6 +57,7 @@ extern "C" {
 int gebq_b200_abi_version(void) { return GEBQ_B200_ABI_VERSION; }
 const char *gebq_b200_last_error(void) { return g_err.c_str(); }
 int gebq_b200_sm_count(void) { return sm_count(); }
+unsigned long long gebq_b200_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 // ---- quantize ---------------------------------------------------------------
 int gebq_quantize_abs_f32(const uint32_t *x, uint32_t *codes, uint8_t *lossless, int64_t n,
@@ -260,29 +266,33 @@ int gebq_validate_index(const int64_t *offsets, int64_t nblocks, int64_t region_
 }
 
 #define DEC_CFG(MODE, SINK) \
-    DecodeCfg d{MODE, SINK, count, block_size, 0, nblocks, nblocks, region_len};
+    DecodeCfg d{MODE, SINK, count, block_size, 0, nblocks, nblocks, region_len, region_len_dev, derived_dev};
 
-int gebq_decode_abs_f32(const uint8_t *region, int64_t region_len, const int64_t *offsets, int64_t nblocks,
-                        int64_t count, int64_t block_size, float eb2, uint32_t *out,
-                        unsigned long long *err_key, void *stream) {
+int gebq_decode_abs_f32(const uint8_t *region, int64_t region_len, const long long *region_len_dev,
+                        const int64_t *offsets, int64_t nblocks, int64_t count, int64_t block_size,
+                        float eb2, const void *derived_dev, uint32_t *out, unsigned long long *err_key,
+                        void *stream) {
     DEC_CFG(MODE_ABS, 1)
     return launch_decode<float>(d, region, offsets, eb2, out, nullptr, err_key, S(stream));
 }
-int gebq_decode_abs_f64(const uint8_t *region, int64_t region_len, const int64_t *offsets, int64_t nblocks,
-                        int64_t count, int64_t block_size, double eb2, uint64_t *out,
-                        unsigned long long *err_key, void *stream) {
+int gebq_decode_abs_f64(const uint8_t *region, int64_t region_len, const long long *region_len_dev,
+                        const int64_t *offsets, int64_t nblocks, int64_t count, int64_t block_size,
+                        double eb2, const void *derived_dev, uint64_t *out, unsigned long long *err_key,
+                        void *stream) {
     DEC_CFG(MODE_ABS, 1)
     return launch_decode<double>(d, region, offsets, eb2, out, nullptr, err_key, S(stream));
 }
-int gebq_decode_rel_f32(const uint8_t *region, int64_t region_len, const int64_t *offsets, int64_t nblocks,
-                        int64_t count, int64_t block_size, float w, uint32_t *out,
-                        unsigned long long *err_key, void *stream) {
+int gebq_decode_rel_f32(const uint8_t *region, int64_t region_len, const long long *region_len_dev,
+                        const int64_t *offsets, int64_t nblocks, int64_t count, int64_t block_size,
+                        float w, const void *derived_dev, uint32_t *out, unsigned long long *err_key,
+                        void *stream) {
     DEC_CFG(MODE_REL, 1)
     return launch_decode<float>(d, region, offsets, w, out, nullptr, err_key, S(stream));
 }
-int gebq_decode_rel_f64(const uint8_t *region, int64_t region_len, const int64_t *offsets, int64_t nblocks,
-                        int64_t count, int64_t block_size, double w, uint64_t *out,
-                        unsigned long long *err_key, void *stream) {
+int gebq_decode_rel_f64(const uint8_t *region, int64_t region_len, const long long *region_len_dev,
+                        const int64_t *offsets, int64_t nblocks, int64_t count, int64_t block_size,
+                        double w, const void *derived_dev, uint64_t *out, unsigned long long *err_key,
+                        void *stream) {
     DEC_CFG(MODE_REL, 1)
     return launch_decode<double>(d, region, offsets, w, out, nullptr, err_key, S(stream));
 }
@@ -291,13 +301,13 @@ int gebq_decode_rel_f64(const uint8_t *region, int64_t region_len, const int64_t
 int gebq_decode_blocks_u32(const uint8_t *buf, const int64_t *offsets, int64_t noffsets, int64_t region_end,
                            int64_t count, int64_t block_size, int64_t b0, int64_t b1, uint32_t *codes,
                            uint8_t *lossless, unsigned long long *err_key, void *stream) {
-    DecodeCfg d{MODE_ABS, 0, count, block_size, b0, b1, noffsets, region_end};
+    DecodeCfg d{MODE_ABS, 0, count, block_size, b0, b1, noffsets, region_end, nullptr, nullptr};
     return launch_decode<float>(d, buf, offsets, 0.0f, codes, lossless, err_key, S(stream));
 }
 int gebq_decode_blocks_u64(const uint8_t *buf, const int64_t *offsets, int64_t noffsets, int64_t region_end,
                            int64_t count, int64_t block_size, int64_t b0, int64_t b1, uint64_t *codes,
                            uint8_t *lossless, unsigned long long *err_key, void *stream) {
-    DecodeCfg d{MODE_ABS, 0, count, block_size, b0, b1, noffsets, region_end};
+    DecodeCfg d{MODE_ABS, 0, count, block_size, b0, b1, noffsets, region_end, nullptr, nullptr};
     return launch_decode<double>(d, buf, offsets, 0.0, codes, lossless, err_key, S(stream));
 }
 int gebq_block_sizes_u32(const uint32_t *codes, int64_t count, int64_t block_size, int64_t b0, int64_t b1,

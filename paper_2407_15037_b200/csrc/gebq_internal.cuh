@@ -19,7 +19,8 @@ inline bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
 // error state (thread-local text, returned codes are negative)
 int set_error(cudaError_t e, const char *what);
 int set_error_msg(int code, const char *msg);
-int check_launch(const char *what);
+int check_launch(const char *what);   // also counts one kernel launch
+void note_launch(int k);                // count k further launches
 
 // SM count x resident CTAs of kThreads (queried once per device)
 int sm_count();

@@ -38,6 +38,8 @@ struct DecodeCfg {
     int64_t b0, b1;
     int64_t noffsets;
     int64_t region_end;
+    const long long *region_end_dev;  // optional: region length produced on the device
+    const void *derived_dev;          // optional: eb2 / w produced on the device (value width)
 };
 
 template <typename T>

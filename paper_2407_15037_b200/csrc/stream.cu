@@ -464,6 +464,8 @@ __global__ void __launch_bounds__(kThreads) k_decode_par(DecodeCfg d, const uint
     uint16_t *tpos = reinterpret_cast<uint16_t *>(smem + buf_bytes);
     __shared__ uint32_t s_wsum[kWarps];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (d.region_end_dev) d.region_end = *d.region_end_dev;
+    if (d.derived_dev) derived = *reinterpret_cast<const T *>(d.derived_dev);
 
     for (int64_t b = d.b0 + blockIdx.x; b < d.b1; b += gridDim.x) {
         const int64_t s = b * d.block_size;
@@ -574,6 +576,8 @@ __global__ void __launch_bounds__(kThreads) k_decode_seq(DecodeCfg d, const uint
     using X = W<T>;
     using U = typename X::U;
     constexpr int MAXL = X::kMaxVarint;
+    if (d.region_end_dev) d.region_end = *d.region_end_dev;
+    if (d.derived_dev) derived = *reinterpret_cast<const T *>(d.derived_dev);
     for (int64_t b = d.b0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < d.b1;
          b += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = b * d.block_size;
@@ -686,6 +690,7 @@ static int gen_dispatch(const EncodeCfg &cfg, const typename W<T>::U *x, const u
         x, fin, k, kdev, cfg.n, cfg.block_size, 0, nblocks, offs, region, index, cfg.base_offset,
         kSrc == 0 ? trig : nullptr);
     k_region_len<<<1, 1, 0, st>>>(offs, sizes, nblocks, region_len);
+    note_launch(2);  // sizes + emit (+ this one below)
     return check_launch("encode (generic)");
 }
 

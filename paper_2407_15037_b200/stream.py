@@ -157,11 +157,15 @@ def header_for(cfg: QuantConfig, count: int, value_range=None) -> StreamHeader:
 
 def decode_values(stream_dev: torch.Tensor, header: StreamHeader, nblocks: int, *,
                   out: Optional[torch.Tensor] = None, err: Optional[torch.Tensor] = None,
-                  index_pos: int = HEADER_SIZE + 8):
+                  index_pos: int = HEADER_SIZE + 8,
+                  region_len_dev: Optional[torch.Tensor] = None,
+                  derived_dev: Optional[torch.Tensor] = None):
     """Fused unpack + reconstruct of a device-resident stream -> value bits.
 
     The index must already be validated (container.parse_layout or
-    :func:`validate_index`).  Returns (values int tensor, err_key int64[1]).
+    :func:`validate_index`).  ``region_len_dev`` / ``derived_dev`` let the
+    decode consume the encoder's device-side outputs (region length, NOA eb2)
+    with no host round trip.  Returns (values int tensor, err_key int64[1]).
     """
     width = header.width
     dev = stream_dev.device
@@ -177,8 +181,11 @@ def decode_values(stream_dev: torch.Tensor, header: StreamHeader, nblocks: int, 
     sfx = "f32" if width == 32 else "f64"
     F = ctypes.c_float if width == 32 else ctypes.c_double
     if header.count:
-        _lib.call(f"gebq_decode_{kind}_{sfx}", _p(region), region_len, _p(offsets), nblocks,
-                  header.count, header.block_size, F(header.derived_value), _p(out), _p(err), _s())
+        rl = _p(region_len_dev) if region_len_dev is not None else ctypes.c_void_p(0)
+        dd = _p(derived_dev) if derived_dev is not None else ctypes.c_void_p(0)
+        _lib.call(f"gebq_decode_{kind}_{sfx}", _p(region), region_len, rl, _p(offsets), nblocks,
+                  header.count, header.block_size, F(header.derived_value), dd, _p(out), _p(err),
+                  _s())
     return out, err
 
 
