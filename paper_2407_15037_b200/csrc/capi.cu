@@ -1,6 +1,7 @@
 // capi.cu -- extern "C" entry points of libgebq_b200.so (include/gebq_b200.h).
 // Thin: argument plumbing + error text; all work is in the kernel files.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <string>
@@ -45,6 +46,11 @@ int sm_count() {
     return cached[dev];
 }
 int resident_grid() { return sm_count() * (2048 / kThreads); }
+
+bool force_generic_kernels() {
+    const char *v = getenv("GEBQ_B200_GENERIC");
+    return v && v[0] == '1';
+}
 
 }  // namespace gebq
 

@@ -68,6 +68,8 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename W<T>::U *_
                                                        unsigned long long *trig, int vec_ok) {
     using U = typename W<T>::U;
     if (kdev) k = *kdev;  // NOA: constants derived on device from the global range
+    RelFast<T> f{};
+    if constexpr (kMode == MODE_REL) f = make_rel_fast<T>(k);
     uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
     auto count = [&](int tr) {
         c0 += tr == TRIG_NAN; c1 += tr == TRIG_INF; c2 += tr == TRIG_GUARD; c3 += tr == TRIG_DCHECK;
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename W<T>::U *_
 #pragma unroll
             for (int s = 0; s < 4; s++) {
                 U c;
-                int tr = quantize_one<T, kMode, kUnsafe>(v[r][s], k, c);
+                int tr = quantize_one_fast<T, kMode, kUnsafe>(v[r][s], k, f, c);
                 v[r][s] = c;
                 fl |= (uint32_t)(tr != TRIG_NONE) << (8 * s);
                 count(tr);
@@ -99,7 +101,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename W<T>::U *_
     for (int64_t i = start + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         U c;
-        int tr = quantize_one<T, kMode, kUnsafe>(x[i], k, c);
+        int tr = quantize_one_fast<T, kMode, kUnsafe>(x[i], k, f, c);
         codes[i] = c;
         flags[i] = tr != TRIG_NONE;
         count(tr);
@@ -243,7 +245,8 @@ __global__ void k_noa_derive(const long long *keys2, double eb, Consts<T> *kout,
 // per-thread pattern count below 2^16).
 // ---------------------------------------------------------------------------
 template <typename T, int kMode, bool kUnsafe>
-__device__ __forceinline__ int sweep_outcome(typename W<T>::U xb, const Consts<T> &k) {
+__device__ __forceinline__ int sweep_outcome(typename W<T>::U xb, const Consts<T> &k,
+                                             const RelFast<T> &f) {
     using X = W<T>;
     using U = typename X::U;
     T xf = X::from_bits(xb);
@@ -259,26 +262,14 @@ __device__ __forceinline__ int sweep_outcome(typename W<T>::U xb, const Consts<T
         if (!kUnsafe && !(err <= k.a)) return 1;
         return err <= k.a ? 0 : 2;
     } else {
-        U ab = xb & X::kAbsMask;
-        int64_t aexpo = (int64_t)(ab >> X::kMantBits);
-        if (xf != xf || aexpo == (int64_t)X::kExpAll || aexpo == 0) return 1;
-        T frac = X::from_bits(((U)X::kBias << X::kMantBits) | (ab & X::kMantMask));
-        T l = X::add(frac, (T)(aexpo - (X::kBias + 1)));
-        T t = X::div(l, k.b);
-        if (!(X::fabs_(t) < k.thr)) return 1;
-        T kf;
-        int64_t kb = round_bin(t, kf);
-        if (kb >= X::kMaxBin || kb <= -X::kMaxBin) return 1;
-        T p = X::mul(kf, k.b);
-        T biased = X::add(p, (T)X::kBias);
-        if (!(biased >= T(1) && biased < (T)(2 * X::kBias + 1))) return 1;
-        int64_t expo = X::trunc_i64(biased);
-        T rfrac = X::sub(biased, (T)(expo - 1));
-        T recon_mag = pow2_assemble<T>(expo, rfrac);
-        T q = X::div(recon_mag, X::fabs_(xf));
-        bool ok = q <= k.a && X::mul(q, k.a) >= T(1);
-        if (!kUnsafe && !ok) return 1;
-        return ok ? 0 : 2;
+        // lossless decision from the production (filtered) quantizer; the
+        // verdict recomputes the exact IEEE predicate on the reconstruction,
+        // so the tallies check the filter against the reference exhaustively
+        U code;
+        if (quantize_rel_fast<T, kUnsafe>(xb, k, f, code) != TRIG_NONE) return 1;
+        U rb = reconstruct_one<T, MODE_REL>(code, false, k.b);
+        T q = X::div(X::fabs_(X::from_bits(rb)), X::fabs_(xf));
+        return (q <= k.a && X::mul(q, k.a) >= T(1)) ? 0 : 2;
     }
 }
 
@@ -312,6 +303,8 @@ __global__ void __launch_bounds__(kThreads) k_sweep(uint64_t start, int64_t coun
                                                     unsigned long long *first_viol,
                                                     int64_t idx_base) {
     using U = typename W<T>::U;
+    RelFast<T> f{};
+    if constexpr (kMode == MODE_REL) f = make_rel_fast<T>(k);
     Tally16 tl;
     uint64_t first = ~0ull;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -321,7 +314,7 @@ __global__ void __launch_bounds__(kThreads) k_sweep(uint64_t start, int64_t coun
         if constexpr (kSource == 0) xb = (U)(start + (uint64_t)i);
         else if constexpr (kSource == 1) xb = bits[i];
         else xb = (U)splitmix64_at(seed, start + (uint64_t)i + 1);
-        int o = sweep_outcome<T, kMode, kUnsafe>(xb, k);
+        int o = sweep_outcome<T, kMode, kUnsafe>(xb, k, f);
         tl.add(value_class<T>(xb) * 3 + o);
         if (o == 2 && (uint64_t)i < first) first = (uint64_t)i;
     }

@@ -22,6 +22,10 @@ int set_error_msg(int code, const char *msg);
 int check_launch(const char *what);   // also counts one kernel launch
 void note_launch(int k);                // count k further launches
 
+// GEBQ_B200_GENERIC=1 routes block_size 4096 through the generic stream kernels
+// (used by the tests to cover both code paths on the same inputs)
+bool force_generic_kernels();
+
 // SM count x resident CTAs of kThreads (queried once per device)
 int sm_count();
 int resident_grid();

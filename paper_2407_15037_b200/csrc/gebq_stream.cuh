@@ -47,6 +47,14 @@ int launch_decode(const DecodeCfg &cfg, const uint8_t *region, const int64_t *of
                   void *out_codes, uint8_t *out_flags, unsigned long long *err_key,
                   cudaStream_t st);
 
+template <typename T>
+int launch_encode4k(const EncodeCfg &cfg, const void *x, const Consts<T> &k, const Consts<T> *kdev,
+                    uint8_t *region, uint64_t *index, void *ws, unsigned long long *trig,
+                    long long *region_len, cudaStream_t st);
+template <typename T>
+int launch_decode4k(const DecodeCfg &d, const uint8_t *region, const int64_t *offsets, T derived,
+                    void *out_codes, uint8_t *out_flags, unsigned long long *err_key, cudaStream_t st);
+
 int launch_validate_index(const int64_t *offsets, int64_t nblocks, int64_t region_len, int *flags3,
                           cudaStream_t st);
 

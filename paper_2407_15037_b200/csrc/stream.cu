@@ -717,6 +717,8 @@ int launch_encode(const EncodeCfg &cfg, const void *x, const uint8_t *flags_in, 
         return cfg.unsafe ? GEN(0, MODE_ABS, true) : GEN(0, MODE_ABS, false);
 #undef GEN
     }
+    if (cfg.block_size == kEncTileMax && cfg.src == 0 && !force_generic_kernels())
+        return launch_encode4k<T>(cfg, x, k, kdev, region, index, ws, trig, region_len, st);
     EncArgs<T> a;
     a.x = xp;
     a.fin = flags_in;
@@ -768,6 +770,8 @@ static int decode_dispatch(const DecodeCfg &d, const uint8_t *region, const int6
                            void *oc, uint8_t *of, unsigned long long *err, cudaStream_t st) {
     const int64_t nblk = d.b1 - d.b0;
     if (nblk <= 0) return 0;
+    if (d.block_size == kEncTileMax && !force_generic_kernels())
+        return launch_decode4k<T>(d, region, offsets, derived, oc, of, err, st);
     if (d.block_size >= 64 && d.block_size <= kEncTileMax) {
         const int maxl = W<T>::kMaxVarint;
         const int bmb = (int)(((d.block_size + 63) / 64) * 8);

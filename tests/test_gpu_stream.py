@@ -23,7 +23,17 @@ def _cfg(mode, eb, width=32, vr=None, unsafe=False, bs=4096):
                        block_size=bs)
 
 
-def test_golden_digest(cuda, oracle, golden_record):
+@pytest.fixture(params=["fast", "generic"])
+def kernel_path(request, monkeypatch):
+    """Run a test on the specialised 4096-block kernels and on the generic ones."""
+    if request.param == "generic":
+        monkeypatch.setenv("GEBQ_B200_GENERIC", "1")
+    else:
+        monkeypatch.delenv("GEBQ_B200_GENERIC", raising=False)
+    return request.param
+
+
+def test_golden_digest(cuda, oracle, golden_record, kernel_path):
     import paper_2407_15037_b200 as g
 
     overall = hashlib.sha256()
@@ -99,7 +109,7 @@ def _outcome(fn, data):
         return type(e).__name__ + ":" + str(e)
 
 
-def test_decode_fuzz_typed_errors(cuda, fixtures, fuzz_arrays):
+def test_decode_fuzz_typed_errors(cuda, fixtures, fuzz_arrays, kernel_path):
     """12000 byte mutations: same exception class AND byte position as the reference."""
     import paper_2407_15037_b200 as g
 
@@ -148,7 +158,7 @@ def test_compress_coded_matches_compress(cuda, oracle):
             assert cfg2.value_range == vr
 
 
-def test_workload_fixtures(cuda, fixtures):
+def test_workload_fixtures(cuda, fixtures, kernel_path):
     import paper_2407_15037_b200 as g
     from paper_2407_15037_b200 import workloads
 
@@ -171,7 +181,7 @@ def test_workload_fixtures(cuda, fixtures):
 
 
 @pytest.mark.parametrize("width", [32, 64])
-def test_large_c2_and_noa_vs_oracle(cuda, oracle, width):
+def test_large_c2_and_noa_vs_oracle(cuda, oracle, width, kernel_path):
     """2^24-value streams (mixed REL; planted-extreme NOA) byte-identical to the oracle."""
     import paper_2407_15037_b200 as g
     from paper_2407_15037_b200 import workloads
