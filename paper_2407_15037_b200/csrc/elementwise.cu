@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename W<T>::U *_
 #pragma unroll
             for (int s = 0; s < 4; s++) {
                 U c;
-                int tr = quantize_one_fast<T, kMode, kUnsafe>(v[r][s], k, f, c);
+                int tr = quantize_bf<T, kMode, kUnsafe>(v[r][s], k, f, c);
                 v[r][s] = c;
                 fl |= (uint32_t)(tr != TRIG_NONE) << (8 * s);
                 count(tr);
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename W<T>::U *_
     for (int64_t i = start + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         U c;
-        int tr = quantize_one_fast<T, kMode, kUnsafe>(x[i], k, f, c);
+        int tr = quantize_bf<T, kMode, kUnsafe>(x[i], k, f, c);
         codes[i] = c;
         flags[i] = tr != TRIG_NONE;
         count(tr);
@@ -266,7 +266,7 @@ __device__ __forceinline__ int sweep_outcome(typename W<T>::U xb, const Consts<T
         // verdict recomputes the exact IEEE predicate on the reconstruction,
         // so the tallies check the filter against the reference exhaustively
         U code;
-        if (quantize_rel_fast<T, kUnsafe>(xb, k, f, code) != TRIG_NONE) return 1;
+        if (quantize_rel_bf<T, kUnsafe>(xb, k, f, code) != TRIG_NONE) return 1;
         U rb = reconstruct_one<T, MODE_REL>(code, false, k.b);
         T q = X::div(X::fabs_(X::from_bits(rb)), X::fabs_(xf));
         return (q <= k.a && X::mul(q, k.a) >= T(1)) ? 0 : 2;

@@ -47,6 +47,7 @@ int launch_decode(const DecodeCfg &cfg, const uint8_t *region, const int64_t *of
                   void *out_codes, uint8_t *out_flags, unsigned long long *err_key,
                   cudaStream_t st);
 
+size_t encode4k_workspace_bytes(int64_t n, int width);
 template <typename T>
 int launch_encode4k(const EncodeCfg &cfg, const void *x, const Consts<T> &k, const Consts<T> *kdev,
                     uint8_t *region, uint64_t *index, void *ws, unsigned long long *trig,

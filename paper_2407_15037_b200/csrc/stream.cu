@@ -642,8 +642,15 @@ int64_t encode_region_capacity(int64_t n, int64_t bs, int width) {
 static int64_t blocks_per_tile(int64_t bs) { return bs <= kEncTileMax ? kEncTileMax / bs : 1; }
 
 size_t encode_workspace_bytes(int64_t n, int64_t bs, int width) {
-    (void)width;
     const int64_t nblocks = n ? (n + bs - 1) / bs : 0;
+    if (bs == kEncTileMax) {
+        // specialised path (slots + totals + offsets); also covers the generic one
+        const int64_t V = kEncTileMax;
+        const int64_t ntiles = (n + V - 1) / V;
+        const size_t gen = (size_t)(ntiles + 2) * 8 + 256;
+        const size_t fast = encode4k_workspace_bytes(n, width);
+        return fast > gen ? fast : gen;
+    }
     if (bs <= kEncTileMax) {
         const int64_t V = blocks_per_tile(bs) * bs;
         const int64_t ntiles = (n + V - 1) / V;

@@ -1,0 +1,137 @@
+"""Host <-> device movement for the host-buffer API (compress / decompress_to_array).
+
+The GPU kernels take ~1 ms for 2^26 values; at the user-facing API the cost is
+the PCIe traffic and host copies.  This module keeps both links busy:
+
+* host->device: pinned sources go straight to the copy engine; pageable
+  sources (numpy arrays, ``bytes``) are staged through a ring of pinned chunks
+  with a multi-threaded host copy (torch's parallel memcpy), overlapped with
+  the DMA of the previous chunk.
+* device->host into a fresh ``bytes`` object: the result object is allocated
+  uninitialised (PyBytes_FromStringAndSize(NULL, n), the documented way to
+  build a bytes in place before it is shared), and filled chunk by chunk from a
+  pinned ring while the next chunk is in flight -- no ``tobytes()`` copy.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+import torch
+
+CHUNK = 32 << 20  # bytes per staging chunk
+NSLOTS = 2
+
+_PyBytes_FromStringAndSize = ctypes.pythonapi.PyBytes_FromStringAndSize
+_PyBytes_FromStringAndSize.restype = ctypes.py_object
+_PyBytes_FromStringAndSize.argtypes = [ctypes.c_char_p, ctypes.c_ssize_t]
+
+_tls = threading.local()
+
+
+def _ring(device) -> tuple:
+    """Per-thread pinned staging ring + copy streams for ``device``."""
+    key = ("ring", device.index if device.index is not None else torch.cuda.current_device())
+    r = getattr(_tls, "rings", None)
+    if r is None:
+        r = _tls.rings = {}
+    if key not in r:
+        slots = [torch.empty(CHUNK, dtype=torch.uint8, pin_memory=True) for _ in range(NSLOTS)]
+        events = [torch.cuda.Event() for _ in range(NSLOTS)]
+        r[key] = (slots, events, torch.cuda.Stream(device=device))
+    return r[key]
+
+
+def _is_pinned(t: torch.Tensor) -> bool:
+    try:
+        return t.is_pinned()
+    except Exception:
+        return False
+
+
+def new_bytes(n: int):
+    """An uninitialised bytes object of length n and a writable uint8 CPU tensor over it."""
+    b = _PyBytes_FromStringAndSize(None, n)
+    if n == 0:
+        return b, torch.empty(0, dtype=torch.uint8)
+    addr = ctypes.cast(ctypes.c_char_p(b), ctypes.c_void_p).value
+    arr = np.ctypeslib.as_array((ctypes.c_uint8 * n).from_address(addr))
+    return b, torch.from_numpy(arr)
+
+
+def h2d(src: torch.Tensor, dst: torch.Tensor) -> None:
+    """Copy a uint8 CPU tensor into a uint8 CUDA tensor on the current stream."""
+    n = src.numel()
+    if n == 0:
+        return
+    if _is_pinned(src) or n <= (1 << 20):
+        dst.copy_(src, non_blocking=_is_pinned(src))
+        return
+    cur = torch.cuda.current_stream(dst.device)
+    slots, events, _ = _ring(dst.device)
+    for i, off in enumerate(range(0, n, CHUNK)):
+        k = i % NSLOTS
+        m = min(CHUNK, n - off)
+        events[k].synchronize()                 # slot's previous DMA done
+        slots[k][:m].copy_(src[off:off + m])    # parallel host memcpy into pinned
+        dst[off:off + m].copy_(slots[k][:m], non_blocking=True)
+        events[k].record(cur)
+
+
+def d2h_into(src: torch.Tensor, dst: torch.Tensor) -> None:
+    """Copy a uint8 CUDA tensor into a (pageable) uint8 CPU tensor, chunk-pipelined."""
+    n = src.numel()
+    if n == 0:
+        return
+    if _is_pinned(dst) or n <= (1 << 20):
+        dst.copy_(src)
+        return
+    cur = torch.cuda.current_stream(src.device)
+    slots, events, _ = _ring(src.device)
+    pending = []
+    for i, off in enumerate(range(0, n, CHUNK)):
+        k = i % NSLOTS
+        m = min(CHUNK, n - off)
+        if len(pending) == NSLOTS:              # drain the oldest chunk before reusing its slot
+            po, pm, pk = pending.pop(0)
+            events[pk].synchronize()
+            dst[po:po + pm].copy_(slots[pk][:pm])
+        slots[k][:m].copy_(src[off:off + m], non_blocking=True)
+        events[k].record(cur)
+        pending.append((off, m, k))
+    for po, pm, pk in pending:
+        events[pk].synchronize()
+        dst[po:po + pm].copy_(slots[pk][:pm])
+
+
+def device_to_new_bytes(src: torch.Tensor, prefix: bytes = b"") -> bytes:
+    """bytes(prefix + src) built in place from device memory."""
+    n = src.numel()
+    b, view = new_bytes(len(prefix) + n)
+    if prefix:
+        view[:len(prefix)].copy_(torch.frombuffer(bytearray(prefix), dtype=torch.uint8))
+    d2h_into(src, view[len(prefix):])
+    return b
+
+
+def host_u8(data) -> torch.Tensor:
+    """Zero-copy uint8 CPU tensor over any bytes-like object or array (read-only use)."""
+    import warnings
+
+    if isinstance(data, torch.Tensor):
+        return data.view(torch.uint8).reshape(-1)
+    if isinstance(data, np.ndarray):
+        data = np.ascontiguousarray(data).reshape(-1).view(np.uint8)
+        if data.flags.writeable:
+            return torch.from_numpy(data)
+    if len(data) == 0:
+        return torch.empty(0, dtype=torch.uint8)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return torch.frombuffer(data, dtype=torch.uint8)
+
+
+def pinned_empty(n: int, dtype=torch.uint8) -> torch.Tensor:
+    return torch.empty(n, dtype=dtype, pin_memory=True)

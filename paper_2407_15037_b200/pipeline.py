@@ -91,13 +91,15 @@ def _as_value_array(values, width: int) -> np.ndarray:
 
 
 def _upload(arr: np.ndarray) -> torch.Tensor:
-    """H2D copy of the value bits (pinned sources go at full link speed)."""
+    """H2D copy of the value bits (pinned sources go at full link speed, pageable
+    ones through the pinned staging ring)."""
+    from . import hostio
+
     dev = device.require_cuda()
-    it = np.int32 if arr.dtype.itemsize == 4 else np.int64
-    src = stream.host_u8(arr.view(np.uint8) if arr.size else np.empty(0, np.uint8))
-    t = torch.empty(arr.size, dtype=torch.int32 if it == np.int32 else torch.int64, device=dev)
+    t = torch.empty(arr.size, dtype=torch.int32 if arr.dtype.itemsize == 4 else torch.int64,
+                    device=dev)
     if arr.size:
-        t.view(torch.uint8).copy_(src)
+        hostio.h2d(hostio.host_u8(arr), t.view(torch.uint8))
     return t
 
 

@@ -126,17 +126,14 @@ def encode_coded(codes: torch.Tensor, lossless: torch.Tensor, block_size: int, *
 
 
 def stream_to_host(enc: Encoded, header: StreamHeader, region_len: Optional[int] = None) -> bytes:
-    """Assemble the final stream bytes: host header + one D2H of index + region."""
+    """Assemble the final stream bytes: host header + index + region, D2H'd in place."""
+    from . import hostio
+
     if region_len is None:
         region_len = int(enc.region_len.item())
     total = enc.region_off + region_len
-    host = torch.empty(total, dtype=torch.uint8, pin_memory=True)
-    if total > HEADER_SIZE + 8:
-        host[HEADER_SIZE + 8:].copy_(enc.buf[HEADER_SIZE + 8:total])
-    arr = host.numpy()
-    arr[:HEADER_SIZE] = np.frombuffer(header.pack(), dtype=np.uint8)
-    arr[HEADER_SIZE:HEADER_SIZE + 8] = np.frombuffer(struct.pack("<Q", enc.nblocks), dtype=np.uint8)
-    return arr.tobytes()
+    prefix = header.pack() + struct.pack("<Q", enc.nblocks)
+    return hostio.device_to_new_bytes(enc.buf[HEADER_SIZE + 8:total], prefix)
 
 
 def header_for(cfg: QuantConfig, count: int, value_range=None) -> StreamHeader:
@@ -216,30 +213,20 @@ def validate_index(stream_dev: torch.Tensor, nblocks: int, index_pos: int = HEAD
 
 
 def host_u8(data) -> torch.Tensor:
-    """Zero-copy uint8 CPU tensor over any bytes-like object (read-only is fine: we only read)."""
-    import warnings
+    from . import hostio
 
-    if isinstance(data, torch.Tensor):
-        return data.view(torch.uint8).reshape(-1)
-    if isinstance(data, np.ndarray):
-        data = data.view(np.uint8).reshape(-1)
-        if data.flags.writeable:
-            return torch.from_numpy(data)
-    if len(data) == 0:
-        return torch.empty(0, dtype=torch.uint8)
-    with warnings.catch_warnings():
-        warnings.simplefilter("ignore")
-        return torch.frombuffer(data, dtype=torch.uint8)
+    return hostio.host_u8(data)
 
 
 def _h2d_stream(data) -> torch.Tensor:
+    from . import hostio
+
     dev = require_cuda()
-    src = host_u8(data)
+    src = hostio.host_u8(data)
     n = src.numel()
     # keep 16 bytes of slack so vector loads near the end stay inside the allocation
     t = torch.empty(n + 16, dtype=torch.uint8, device=dev)
-    if n:
-        t[:n].copy_(src)
+    hostio.h2d(src, t[:n])
     return t[:n]
 
 
