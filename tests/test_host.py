@@ -1,0 +1,140 @@
+"""Host-side logic of the product package on CPU: constants derivation,
+header/index parsing with the reference's typed errors, wire-code helpers."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+from helpers import noa_input
+
+
+def test_derived_constants_match_reference(fixtures):
+    from paper_2407_15037_b200.quantizers import QuantConfig
+
+    for rec in fixtures["constants"]:
+        cfg = QuantConfig(mode=rec["mode"], eb=rec["eb"], width=rec["width"],
+                          value_range=rec["value_range"])
+        d = cfg.derived
+        for key in ("thr", "eb_eff", "eb2", "inv_eb2", "op_eps", "w"):
+            if rec[key] is None:
+                assert getattr(d, key) is None
+                continue
+            v = getattr(d, key)
+            bits = (int(np.float32(v).view(np.uint32)) if rec["width"] == 32
+                    else int(np.float64(v).view(np.uint64)))
+            assert bits == rec[key], (rec, key)
+        assert d.header_bits == rec["header_bits"]
+
+
+def test_config_validation():
+    from paper_2407_15037_b200 import InvalidBound, QuantConfig
+
+    for eb in (0.0, -1.0, float("nan"), float("inf")):
+        with pytest.raises(InvalidBound):
+            QuantConfig(mode="abs", eb=eb)
+    with pytest.raises(ValueError):
+        QuantConfig(mode="pwr", eb=1e-3)
+    with pytest.raises(ValueError):
+        QuantConfig(mode="abs", eb=1e-3, width=16)
+    with pytest.raises(ValueError):
+        QuantConfig(mode="noa", eb=1e-3).derived
+    with pytest.raises(ValueError):
+        QuantConfig(mode="abs", eb=1e-3, block_size=0)
+
+
+def test_det_log2_known_values():
+    from paper_2407_15037_b200.quantizers import det_log2
+
+    assert float(det_log2(2.0)) == 1.0
+    assert float(det_log2(4.0, 32)) == 2.0
+    with pytest.raises(ValueError):
+        det_log2(1.0)
+
+
+def test_header_roundtrip_and_errors():
+    from paper_2407_15037_b200.container import (HEADER_SIZE, BadMagic, BadVersion, CorruptHeader,
+                                                 StreamHeader, TruncatedStream)
+
+    h = StreamHeader(width=64, mode="noa", count=5, eb_bits=int(np.float64(0.25).view(np.uint64)),
+                     derived_bits=int(np.float64(0.5).view(np.uint64)),
+                     range_bits=int(np.float64(10.0).view(np.uint64)), block_size=7, flags=1)
+    raw = h.pack()
+    assert len(raw) == HEADER_SIZE and raw[:4] == b"GEBQ"
+    h2 = StreamHeader.unpack(raw)
+    assert h2 == h and h2.eb == 0.25 and h2.value_range == 10.0
+    assert float(h2.derived_value) == 0.5 and h2.double_check_disabled
+    for pos, val, exc in ((0, ord("X"), BadMagic), (4, 99, BadVersion), (6, 7, CorruptHeader),
+                          (7, 9, CorruptHeader)):
+        b = bytearray(raw)
+        b[pos] = val
+        with pytest.raises(exc):
+            StreamHeader.unpack(bytes(b))
+    with pytest.raises(TruncatedStream):
+        StreamHeader.unpack(raw[:47])
+
+
+def test_index_validation_matches_reference_on_fuzz(fixtures, fuzz_arrays):
+    """Every mutation the reference rejects before decoding blocks is rejected by
+    parse_layout with the same class and message; the rest pass through."""
+    from paper_2407_15037_b200.container import ContainerError, parse_layout
+
+    block_level = ("payload ends mid-block", "non-canonical or out-of-range varint",
+                   "block extent does not match")
+    checked = 0
+    for meta in fixtures["decode_fuzz"]:
+        base = fuzz_arrays[meta["name"] + "_base"].tobytes()
+        for m, expect in zip(fuzz_arrays[meta["name"] + "_muts"], meta["outcomes"]):
+            s = bytearray(base)
+            for p, x in m:
+                if p >= 0:
+                    s[p] ^= int(x)
+            try:
+                parse_layout(bytes(s))
+                assert expect.startswith("OK") or any(b in expect for b in block_level), expect
+            except ContainerError as e:
+                assert type(e).__name__ + ":" + str(e) == expect
+                checked += 1
+    assert checked > 100
+
+
+def test_wire_code_helpers():
+    from paper_2407_15037_b200.container import (coded_array_from_values, unzigzag,
+                                                 values_from_coded_array, zigzag)
+    from paper_2407_15037_b200.quantizers import CodedValue
+
+    assert [zigzag(v) for v in (0, -1, 1, -2, 2)] == [0, 1, 2, 3, 4]
+    for v in (0, 5, -7, 2**29, -(2**29)):
+        assert unzigzag(zigzag(v)) == v
+    vals = [CodedValue.quantized(3), CodedValue.from_raw(0x7FC00000), CodedValue.quantized(-1, 1)]
+    ca = coded_array_from_values(vals, "rel", 32)
+    assert values_from_coded_array(ca) == vals
+
+
+def test_c2_recipe_matches_fixture(fixtures):
+    from paper_2407_15037_b200 import workloads
+
+    rec = [r for r in fixtures["workloads"] if r["workload"] == "c2"][0]
+    x = workloads.c2_values(rec["n"])
+    assert hashlib.sha256(x.tobytes()).hexdigest() == rec["input_sha256"]
+
+
+def test_noa_inputs_decode(fixtures):
+    for rec in fixtures["noa"]:
+        arr = noa_input(rec)
+        assert arr.dtype.name == rec["dtype"]
+
+
+def test_no_cpu_fallback_without_gpu():
+    """The product path must fail loudly without a CUDA device, never fall back."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import paper_2407_15037_b200 as g
+    from paper_2407_15037_b200.device import NoDeviceError
+
+    with pytest.raises(NoDeviceError):
+        g.compress(np.ones(10, np.float32), g.QuantConfig(mode="abs", eb=1e-3))
+    with pytest.raises(NoDeviceError):
+        g.sweep_f32("abs", [1e-3], count=100)
