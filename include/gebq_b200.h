@@ -217,6 +217,30 @@ int gebq_decode_rel_f64(const uint8_t *region, int64_t region_len,
                         const long long *region_len_dev, const int64_t *offsets, int64_t nblocks,
                         int64_t count, int64_t block_size, double w, const void *derived_dev,
                         uint64_t *out, unsigned long long *err_key, void *stream);
+/* Self-check of the division-free REL filter inside the f32 stream encoder:
+ * for patterns [start, start+count) mod 2^32, out2[0] += values whose
+ * certified fast-path (code, trigger) differs from the reference op sequence
+ * (quantize_rel32, _kernels.py:165-224) -- must stay 0 -- and out2[1] +=
+ * values deferred to the exact sequence.                                    */
+int gebq_selfcheck_rel_filter_f32(uint64_t start, int64_t count, float op_eps, float w, float thr,
+                                  int unsafe, unsigned long long *out2, void *stream);
+
+/* decode_span_*: the fused decode restricted to blocks [b0, b1) of a stream
+ * (same region / offsets / count as the whole-stream call; outputs land at
+ * their absolute value positions).  Lets the host API decode early blocks
+ * while later stream bytes are still being copied in.                      */
+int gebq_decode_span_abs_f32(const uint8_t *region, int64_t region_len, const int64_t *offsets,
+                             int64_t nblocks, int64_t count, int64_t block_size, float eb2, int64_t b0,
+                             int64_t b1, uint32_t *out, unsigned long long *err_key, void *stream);
+int gebq_decode_span_abs_f64(const uint8_t *region, int64_t region_len, const int64_t *offsets,
+                             int64_t nblocks, int64_t count, int64_t block_size, double eb2, int64_t b0,
+                             int64_t b1, uint64_t *out, unsigned long long *err_key, void *stream);
+int gebq_decode_span_rel_f32(const uint8_t *region, int64_t region_len, const int64_t *offsets,
+                             int64_t nblocks, int64_t count, int64_t block_size, float w, int64_t b0,
+                             int64_t b1, uint32_t *out, unsigned long long *err_key, void *stream);
+int gebq_decode_span_rel_f64(const uint8_t *region, int64_t region_len, const int64_t *offsets,
+                             int64_t nblocks, int64_t count, int64_t block_size, double w, int64_t b0,
+                             int64_t b1, uint64_t *out, unsigned long long *err_key, void *stream);
 int gebq_decode_blocks_u32(const uint8_t *buf, const int64_t *offsets, int64_t noffsets,
                            int64_t region_end, int64_t count, int64_t block_size, int64_t b0,
                            int64_t b1, uint32_t *codes, uint8_t *lossless,

@@ -304,6 +304,42 @@ int gebq_decode_rel_f64(const uint8_t *region, int64_t region_len, const long lo
 }
 #undef DEC_CFG
 
+// span variants: blocks [b0, b1) of a stream whose bytes may still be arriving
+// (the host-buffer API pipelines H2D of later blocks behind this decode)
+#define SPAN_CFG(MODE) \
+    DecodeCfg d{MODE, 1, count, block_size, b0, b1, nblocks, region_len, nullptr, nullptr};
+int gebq_decode_span_abs_f32(const uint8_t *region, int64_t region_len, const int64_t *offsets,
+                             int64_t nblocks, int64_t count, int64_t block_size, float eb2, int64_t b0,
+                             int64_t b1, uint32_t *out, unsigned long long *err_key, void *stream) {
+    SPAN_CFG(MODE_ABS)
+    return launch_decode<float>(d, region, offsets, eb2, out, nullptr, err_key, S(stream));
+}
+int gebq_decode_span_abs_f64(const uint8_t *region, int64_t region_len, const int64_t *offsets,
+                             int64_t nblocks, int64_t count, int64_t block_size, double eb2, int64_t b0,
+                             int64_t b1, uint64_t *out, unsigned long long *err_key, void *stream) {
+    SPAN_CFG(MODE_ABS)
+    return launch_decode<double>(d, region, offsets, eb2, out, nullptr, err_key, S(stream));
+}
+int gebq_decode_span_rel_f32(const uint8_t *region, int64_t region_len, const int64_t *offsets,
+                             int64_t nblocks, int64_t count, int64_t block_size, float w, int64_t b0,
+                             int64_t b1, uint32_t *out, unsigned long long *err_key, void *stream) {
+    SPAN_CFG(MODE_REL)
+    return launch_decode<float>(d, region, offsets, w, out, nullptr, err_key, S(stream));
+}
+int gebq_decode_span_rel_f64(const uint8_t *region, int64_t region_len, const int64_t *offsets,
+                             int64_t nblocks, int64_t count, int64_t block_size, double w, int64_t b0,
+                             int64_t b1, uint64_t *out, unsigned long long *err_key, void *stream) {
+    SPAN_CFG(MODE_REL)
+    return launch_decode<double>(d, region, offsets, w, out, nullptr, err_key, S(stream));
+}
+#undef SPAN_CFG
+
+int gebq_selfcheck_rel_filter_f32(uint64_t start, int64_t count, float op_eps, float w, float thr,
+                                  int unsafe, unsigned long long *out2, void *stream) {
+    Consts<float> k{op_eps, w, 0.0f, thr};
+    return launch_check_rel_try(start, count, k, unsafe, out2, S(stream));
+}
+
 int gebq_decode_blocks_u32(const uint8_t *buf, const int64_t *offsets, int64_t noffsets, int64_t region_end,
                            int64_t count, int64_t block_size, int64_t b0, int64_t b1, uint32_t *codes,
                            uint8_t *lossless, unsigned long long *err_key, void *stream) {

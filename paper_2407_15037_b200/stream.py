@@ -257,15 +257,72 @@ def decode_coded_host(data, header: StreamHeader, nblocks: int, index_pos: int):
             lossless.cpu().numpy().view(np.bool_))
 
 
+DECODE_CHUNK = 16 << 20   # stream bytes per pipelined span
+
+
 def decode_values_host(data, header: StreamHeader, nblocks: int, index_pos: int) -> np.ndarray:
+    """Host stream -> host values, PCIe in both directions overlapped with the decode.
+
+    The stream is cut into spans of whole blocks (~DECODE_CHUNK bytes each,
+    from the already validated index): span i's bytes cross PCIe on a copy
+    stream while span i-1 decodes on the compute stream and span i-2's values
+    return on a third stream.  Errors are reduced over all spans into one key
+    (the smallest failing position wins, container.py:308-311) and raised after
+    the last span.
+    """
+    from . import hostio
+
     width = header.width
     ft = np.float32 if width == 32 else np.float64
-    if header.count == 0:
+    count = header.count
+    if count == 0:
         return np.empty(0, ft)
-    sd = _h2d_stream(data)
-    out, err = decode_values(sd, header, nblocks, index_pos=index_pos)
-    host = torch.empty(header.count, dtype=_ITYPE[width], pin_memory=True)
-    host.copy_(out)
-    key = int(err.item()) & ERR_NONE
+    dev = require_cuda()
+    src = hostio.host_u8(data)
+    total = src.numel()
+    region_pos = index_pos + 8 * nblocks
+    region_len = total - region_pos
+    offs = src[index_pos:region_pos].numpy().view("<i8")
+    sd = torch.empty(total + 16, dtype=torch.uint8, device=dev)
+    out = torch.empty(count, dtype=_ITYPE[width], device=dev)
+    host = torch.empty(count, dtype=_ITYPE[width], pin_memory=True)
+    err = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    kind = "rel" if header.mode == REL else "abs"
+    fn = getattr(_lib.load(), f"gebq_decode_span_{kind}_{'f32' if width == 32 else 'f64'}")
+    F = ctypes.c_float if width == 32 else ctypes.c_double
+    derived = F(header.derived_value)
+    bs = header.block_size
+    cur = torch.cuda.current_stream(dev)
+    out_stream = _out_stream(dev)
+    pipe = hostio.H2DPipe(src, sd)
+    region_p, offs_p = sd.data_ptr() + region_pos, sd.data_ptr() + index_pos
+    b0, lo = 0, 0
+    while b0 < nblocks:
+        # next span: whole blocks up to ~DECODE_CHUNK stream bytes past this span's start
+        b1 = int(np.searchsorted(offs, offs[b0] + DECODE_CHUNK, side="left"))
+        b1 = min(max(b1, b0 + 1), nblocks)
+        hi = region_pos + (int(offs[b1]) if b1 < nblocks else region_len)
+        cur.wait_event(pipe.push(lo, hi))
+        rc = fn(region_p, region_len, offs_p, nblocks, count, bs, derived, b0, b1, _p(out),
+                _p(err), _s())
+        if rc != 0:
+            raise _lib.GebqCudaError(f"decode span failed ({rc}): {_lib.last_error()}")
+        v0, v1 = b0 * bs, min(b1 * bs, count)
+        out_stream.wait_stream(cur)
+        with torch.cuda.stream(out_stream):
+            host[v0:v1].copy_(out[v0:v1], non_blocking=True)
+        b0, lo = b1, hi
+    cur.wait_stream(out_stream)
+    key = int(err.item()) & ERR_NONE                 # syncs the compute stream (after all copies)
     raise_for_err_key(key)
     return host.numpy().view(ft)
+
+
+_OUT_STREAMS: dict = {}
+
+
+def _out_stream(dev) -> torch.cuda.Stream:
+    k = dev.index if dev.index is not None else torch.cuda.current_device()
+    if k not in _OUT_STREAMS:
+        _OUT_STREAMS[k] = torch.cuda.Stream(device=dev)
+    return _OUT_STREAMS[k]

@@ -246,3 +246,28 @@ def test_kernel_dropins_vs_oracle(cuda, oracle):
     w = np.empty(1000, np.uint64)
     K.splitmix64_fill(w, 0x9E3779B97F4A7C15, 5)
     np.testing.assert_array_equal(w, oracle.splitmix64_fill(1000, 0x9E3779B97F4A7C15, 5))
+
+
+@pytest.mark.parametrize("eb", [1e-1, 1e-2, 1e-3, 1e-5])
+@pytest.mark.parametrize("unsafe", [False, True])
+def test_rel_filter_exhaustive(cuda, eb, unsafe):
+    """Every f32 pattern: where the stream encoder's division-free REL filter
+    certifies a decision, the (code, trigger) equals the reference op sequence
+    (quantize_rel32, _kernels.py:165-224); undecided values (deferred to that
+    exact sequence) stay a tiny fraction."""
+    import ctypes
+
+    import torch
+
+    from paper_2407_15037_b200 import _lib
+    from paper_2407_15037_b200.quantizers import QuantConfig
+
+    d = QuantConfig(mode="rel", eb=eb, width=32, unsafe_no_double_check=unsafe).derived
+    out = torch.zeros(2, dtype=torch.int64, device="cuda")
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    _lib.call("gebq_selfcheck_rel_filter_f32", 0, 1 << 32, ctypes.c_float(d.op_eps),
+              ctypes.c_float(d.w), ctypes.c_float(d.thr), int(unsafe),
+              ctypes.c_void_p(out.data_ptr()), s)
+    bad, deferred = out.cpu().tolist()
+    assert bad == 0
+    assert deferred < (1 << 32) // 50, deferred
