@@ -77,6 +77,31 @@ def advise_hugepages(addr: int, n: int) -> None:
         _madvise(lo, hi - lo, _MADV_HUGEPAGE)
 
 
+_MADV_POPULATE_WRITE = 23
+
+
+def populate_async(addr: int, n: int, nthreads: int = 8) -> list:
+    """Fault in [addr, addr + n) ahead of use, in background threads.
+
+    madvise(MADV_POPULATE_WRITE) allocates the (zeroed) pages without writing
+    user data, so it may run concurrently with copies into the same range.
+    The page faults of a fresh multi-hundred-MB result otherwise serialise
+    behind the copies that first touch them.  Returns the threads (join them).
+    """
+    if _madvise is None or n < (8 << 20):
+        return []
+    lo = (addr + 4095) & ~4095
+    hi = (addr + n) & ~4095
+    step = max(((hi - lo) // nthreads + (2 << 20) - 1) & ~((2 << 20) - 1), 2 << 20)
+    ths = []
+    for a in range(lo, hi, step):
+        th = threading.Thread(target=_madvise, args=(a, min(step, hi - a), _MADV_POPULATE_WRITE),
+                              daemon=True)
+        th.start()
+        ths.append(th)
+    return ths
+
+
 def new_bytes(n: int):
     """An uninitialised bytes object of length n and a writable uint8 CPU tensor over it."""
     b = _PyBytes_FromStringAndSize(None, n)
@@ -214,3 +239,52 @@ class H2DPipe:
         ev = torch.cuda.Event()
         ev.record(st)
         return ev
+
+
+# --- a bytes result built in place, sized after the fact -------------------
+# PyBytes_FromStringAndSize(NULL, cap) creates an uninitialised object owned by
+# the caller (refcount 1); _PyBytes_Resize shrinks such a brand-new object to
+# its final length (the documented way to build a bytes whose size is only
+# known at the end; realloc of the large block shrinks in place).  Only the
+# touched pages of the capacity are ever backed by memory.
+_bytes_new_raw = ctypes.PYFUNCTYPE(ctypes.c_void_p, ctypes.c_char_p, ctypes.c_ssize_t)(
+    ("PyBytes_FromStringAndSize", ctypes.pythonapi))
+_bytes_as_string = ctypes.PYFUNCTYPE(ctypes.c_void_p, ctypes.c_void_p)(("PyBytes_AsString", ctypes.pythonapi))
+_bytes_resize = ctypes.PYFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), ctypes.c_ssize_t)(
+    ("_PyBytes_Resize", ctypes.pythonapi))
+_py_decref = ctypes.pythonapi.Py_DecRef
+_py_decref.argtypes = [ctypes.c_void_p]
+_py_decref.restype = None
+
+
+class BytesBuilder:
+    """A new ``bytes`` of up to ``cap`` bytes, filled through a writable uint8 view
+    and finalised with :meth:`finish` (which shrinks it to the used length)."""
+
+    def __init__(self, cap: int):
+        self._obj = ctypes.c_void_p(_bytes_new_raw(None, cap))
+        if not self._obj.value:
+            raise MemoryError(f"cannot allocate a {cap}-byte result")
+        self.cap = cap
+        self.addr = _bytes_as_string(self._obj)
+        advise_hugepages(self.addr, cap)
+        arr = np.ctypeslib.as_array((ctypes.c_uint8 * max(cap, 1)).from_address(self.addr))[:cap]
+        self.view = torch.from_numpy(arr)
+
+    def finish(self, n: int) -> bytes:
+        if not 0 <= n <= self.cap:
+            raise ValueError("final length beyond capacity")
+        self.view = None
+        if _bytes_resize(ctypes.byref(self._obj), n) != 0 or not self._obj.value:
+            raise MemoryError("cannot finalise the result bytes")
+        out = ctypes.cast(self._obj, ctypes.py_object).value   # new reference
+        _py_decref(self._obj)                                 # drop the builder's reference
+        self._obj = ctypes.c_void_p(0)
+        return out
+
+    def __del__(self):
+        obj = getattr(self, "_obj", None)
+        if obj is not None and obj.value and _py_decref is not None:
+            self.view = None
+            _py_decref(obj)
+            self._obj = ctypes.c_void_p(0)

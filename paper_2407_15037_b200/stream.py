@@ -12,6 +12,7 @@ Device stream buffer layout (one allocation, so one D2H moves a whole stream):
 from __future__ import annotations
 
 import ctypes
+import os
 import struct
 from dataclasses import dataclass
 from typing import Optional
@@ -102,6 +103,173 @@ def encode(x: torch.Tensor, cfg: QuantConfig, *, consts_dev: Optional[torch.Tens
                   F(d.thr), unsafe, bs, *common)
     return Encoded(buf=buf, nblocks=nblocks, count=n, width=width, region_len=region_len,
                    trig=trig)
+
+
+COMPRESS_CHUNK = 16 << 20   # input bytes per pipelined span (whole blocks)
+D2H_SLOT = 16 << 20
+
+
+def _encode_span(xb: torch.Tensor, cfg: QuantConfig, region_ptr: int, index_ptr: int,
+                 ws: torch.Tensor, trig: torch.Tensor, rl_ptr: int) -> None:
+    """One encode launch over ``xb`` (whole blocks) into explicit output pointers."""
+    width = cfg.width
+    n = xb.numel()
+    sfx = "f32" if width == 32 else "f64"
+    F = ctypes.c_float if width == 32 else ctypes.c_double
+    unsafe = int(bool(cfg.unsafe_no_double_check))
+    d = cfg.derived
+    common = (ctypes.c_void_p(region_ptr), ctypes.c_void_p(index_ptr), 0, _p(ws), ws.numel(),
+              _p(trig), ctypes.c_void_p(rl_ptr), _s())
+    if cfg.mode == REL:
+        _lib.call(f"gebq_encode_rel_{sfx}", _p(xb), n, F(d.op_eps), F(d.w), F(d.thr), unsafe,
+                  cfg.block_size, *common)
+    else:
+        _lib.call(f"gebq_encode_abs_{sfx}", _p(xb), n, F(d.eb_eff), F(d.eb2), F(d.inv_eb2),
+                  F(d.thr), unsafe, cfg.block_size, *common)
+
+
+def compress_pipelined(arr: np.ndarray, cfg: QuantConfig, header: StreamHeader):
+    """Host values -> stream bytes with PCIe in both directions overlapped.
+
+    The array is cut into spans of whole blocks (~COMPRESS_CHUNK bytes).  Span
+    i is copied in on a side stream while span i-1 is encoded; each span's
+    block region returns on a third stream as soon as its length is known and
+    is copied straight into the result ``bytes`` at its final offset, so the
+    result is complete (index entries shifted by the preceding spans'
+    lengths) when the last span lands.  Constants must be known up front (not
+    the NOA range pass).  Returns (stream bytes, trigger counts int64[4]).
+    """
+    from . import hostio
+
+    dev = require_cuda()
+    width = cfg.width
+    W = width // 8
+    n = arr.size
+    bs = cfg.block_size
+    nblocks = -(-n // bs)
+    per = max(bs, (COMPRESS_CHUNK // W) // bs * bs)
+    spans = [(v0, min(v0 + per, n)) for v0 in range(0, n, per)]
+    caps = [region_capacity(v1 - v0, bs, width) for v0, v1 in spans]
+    capoff = np.concatenate([[0], np.cumsum(caps)]).astype(np.int64)
+    src = hostio.host_u8(arr)
+    x = torch.empty(n, dtype=_ITYPE[width], device=dev)
+    xb8 = x.view(torch.uint8)
+    regions = torch.empty(int(capoff[-1]) + 16, dtype=torch.uint8, device=dev)
+    index = torch.empty(max(nblocks, 1), dtype=torch.int64, device=dev)
+    ws = torch.empty(max(workspace_bytes(per, bs, width), 16), dtype=torch.uint8, device=dev)
+    trig = torch.zeros(4, dtype=torch.int64, device=dev)
+    rl = torch.empty(len(spans), dtype=torch.int64, device=dev)
+    rl_host = torch.empty(len(spans), dtype=torch.int64, pin_memory=True)
+    hdr_len = HEADER_SIZE + 8 + 8 * nblocks
+    out = hostio.BytesBuilder(hdr_len + int(capoff[-1]))
+    cur = torch.cuda.current_stream(dev)
+    out_stream = _out_stream(dev)
+    ring = _d2h_ring(dev)
+    pipe = hostio.H2DPipe(src, xb8)
+    enc_ev = []
+
+    def launch(c):
+        v0, v1 = spans[c]
+        cur.wait_event(pipe.push(v0 * W, v1 * W))
+        _encode_span(x[v0:v1], cfg, regions.data_ptr() + int(capoff[c]),
+                     index.data_ptr() + 8 * (v0 // bs), ws, trig, rl.data_ptr() + 8 * c)
+        rl_host[c:c + 1].copy_(rl[c:c + 1], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        enc_ev.append(ev)
+
+    bases = []
+    state = {"base": 0, "k": 0}
+
+    def drain(c):
+        enc_ev[c].synchronize()
+        L = int(rl_host[c])
+        base = state["base"]
+        bases.append(base)
+        src_dev = regions[int(capoff[c]):int(capoff[c]) + L]
+        dst = out.view[hdr_len + base:hdr_len + base + L]
+        _d2h_ring_copy(ring, out_stream, enc_ev[c], src_dev, dst, state)
+        state["base"] = base + L
+
+    populate = []
+
+    def prefault():
+        # size the result from the first span's compression and fault its pages
+        # in while the rest of the input is still crossing PCIe
+        enc_ev[0].synchronize()
+        v0, v1 = spans[0]
+        est = hdr_len + int(int(rl_host[0]) * (n / (v1 - v0)) * 1.1) + (4 << 20)
+        nth = int(os.environ.get("GEBQ_B200_PREFAULT_THREADS", "0"))
+        if nth > 0:
+            populate.extend(hostio.populate_async(out.addr, min(est, out.cap), nth))
+
+    if pipe.pinned:          # every span's copy and encode queued at once
+        for c in range(len(spans)):
+            launch(c)
+        prefault()
+        for c in range(len(spans)):
+            drain(c)
+    else:                    # staging copies interleave with draining the previous span
+        for c in range(len(spans)):
+            launch(c)
+            if c == 0:
+                prefault()
+            if c:
+                drain(c - 1)
+        drain(len(spans) - 1)
+    _d2h_ring_flush(ring, state)
+    for th in populate:
+        th.join()
+    total = state["base"]
+    # index: span-relative entries -> stream offsets
+    if nblocks:
+        out.view[HEADER_SIZE + 8:hdr_len].copy_(index.view(torch.uint8)[:8 * nblocks])
+        idx = out.view[HEADER_SIZE + 8:hdr_len].numpy().view("<u8")
+        for (v0, v1), b in zip(spans, bases):
+            idx[v0 // bs:-(-v1 // bs)] += np.uint64(b)
+    prefix = header.pack() + struct.pack("<Q", nblocks)
+    out.view[:len(prefix)].copy_(torch.frombuffer(bytearray(prefix), dtype=torch.uint8))
+    trig_h = trig.cpu().numpy()
+    return out.finish(hdr_len + total), trig_h
+
+
+_RINGS: dict = {}
+
+
+def _d2h_ring(dev):
+    k = dev.index if dev.index is not None else torch.cuda.current_device()
+    if k not in _RINGS:
+        _RINGS[k] = ([torch.empty(D2H_SLOT, dtype=torch.uint8, pin_memory=True) for _ in range(2)],
+                     [torch.cuda.Event() for _ in range(2)])
+    return _RINGS[k]
+
+
+def _d2h_ring_copy(ring, stream, after: torch.cuda.Event, src: torch.Tensor, dst: torch.Tensor, state):
+    """Device bytes -> pageable host bytes through two pinned slots: the DMA of
+    one slot overlaps the host copy out of the other."""
+    slots, evs = ring
+    pend = state.setdefault("pend", [])
+    stream.wait_event(after)
+    n = src.numel()
+    for off in range(0, n, D2H_SLOT):
+        m = min(D2H_SLOT, n - off)
+        k = state["k"]
+        state["k"] = k ^ 1
+        if len(pend) == 2:                     # the slot about to be reused: finish its host copy
+            pk, pdst, pm = pend.pop(0)
+            evs[pk].synchronize()
+            pdst.copy_(slots[pk][:pm])
+        with torch.cuda.stream(stream):
+            slots[k][:m].copy_(src[off:off + m], non_blocking=True)
+        evs[k].record(stream)
+        pend.append((k, dst[off:off + m], m))
+
+
+def _d2h_ring_flush(ring, state):
+    slots, evs = ring
+    for pk, pdst, pm in state.pop("pend", []):
+        evs[pk].synchronize()
+        pdst.copy_(slots[pk][:pm])
 
 
 def encode_coded(codes: torch.Tensor, lossless: torch.Tensor, block_size: int, *,

@@ -271,3 +271,30 @@ def test_rel_filter_exhaustive(cuda, eb, unsafe):
     bad, deferred = out.cpu().tolist()
     assert bad == 0
     assert deferred < (1 << 32) // 50, deferred
+
+
+@pytest.mark.parametrize("mode,eb,bs,pinned,n", [
+    ("abs", 1e-3, 4096, True, 3 * (1 << 23) + 77),
+    ("rel", 1e-2, 1000, False, 5 * (1 << 22) + 3),
+    ("rel", 1e-3, 4096, True, 1 << 24),
+])
+def test_pipelined_compress_vs_oracle(cuda, oracle, mode, eb, bs, pinned, n):
+    """Large inputs take the span-pipelined compress (PCIe overlapped with the
+    encode); the bytes must equal the one-shot oracle stream exactly."""
+    import torch
+
+    import paper_2407_15037_b200 as g
+    from paper_2407_15037_b200 import stream, workloads
+    from paper_2407_15037_b200.quantizers import QuantConfig
+
+    x = workloads.c2_values(n)
+    assert x.nbytes > 2 * stream.COMPRESS_CHUNK
+    if pinned:
+        t = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        t.numpy()[:] = x.view(np.int32)
+        x = t.numpy().view(np.float32)
+    s, st = g.compress(x, QuantConfig(mode=mode, eb=eb, width=32, block_size=bs))
+    so, trig, _ = oracle.compress(x, mode, eb, block_size=bs, workers=8)
+    assert len(s) == len(so)
+    assert s == so
+    assert trig_list(st.triggers) == list(trig)
