@@ -346,6 +346,20 @@ def main():
     if not os.environ.get("GEBQ_B200_EXP"):
         assert int(err.item()) == -1, "decode reported an error on a freshly encoded stream"
     trig_h = trig.cpu().numpy().tolist()
+    # bound check of the step's round trip on the device (verify.py:88-153)
+    from paper_2407_15037_b200 import verify as verify_values
+
+    ftype = torch.float32 if wl["width"] == 32 else torch.float64
+    vr = None
+    if wl["mode"] == NOA:
+        _, rng_dev = gdev.noa_derive(keys, wl["eb"], wl["width"])
+        vr = float(rng_dev.item())
+    vrep = verify_values(x.view(ftype), out.view(ftype), wl["mode"], wl["eb"], vr)
+    violations = vrep.violations + vrep.special_mismatch_count
+    if world > 1:
+        vt = torch.tensor([violations], dtype=torch.int64, device=dev)
+        dist.all_reduce(vt)
+        violations = int(vt.item())
 
     # timed region: K device steps, events on the launching stream
     events = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
@@ -449,6 +463,8 @@ def main():
                         "decode": {"ms": dec_ms, "gbs": dec_gbs, "frac": dec_gbs / peak,
                                    "bytes": dec_bytes, "input_gbs": n * W / (dec_ms * 1e-3) / 1e9}},
             "stream_bytes_per_value": stream_bytes / n, "triggers": trig_h,
+            "violations": violations,
+            "violations_check": "device verify (verify.py:88-153 predicates) of every decoded value, all ranks",
             "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)

@@ -136,6 +136,18 @@ int gebq_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_in
                        void *stream);
 
 
+/* ---- verify: verify.py:88-153 on the device -------------------------------
+ * rel = 1: bound = op_eps (same sign, q = |r|/|o|, q <= op_eps, q*op_eps >= 1);
+ * rel = 0: bound = eb_eff (|o - r| <= eb_eff; ABS and NOA).  NaN/Inf
+ * originals must match bit-exactly.  out5 = {violations (+=), special
+ * mismatches (+=), first violation index (min; preset UINT64_MAX), max error
+ * (|o-r| or |q-1| as binary64 bits, max; preset 0), unused}.  mask (optional,
+ * n bytes): 1 violation, 2 special mismatch, 0 otherwise.                  */
+int gebq_verify_f32(const uint32_t *original, const uint32_t *recon, int64_t n, int rel, float bound,
+                    unsigned long long *out5, uint8_t *mask, void *stream);
+int gebq_verify_f64(const uint64_t *original, const uint64_t *recon, int64_t n, int rel, double bound,
+                    unsigned long long *out5, uint8_t *mask, void *stream);
+
 /* ---- stream encode: quantize + pack into FORMAT.md in ONE pass ------------
  * Replaces quantize_* + block_sizes_* + cumsum + emit_blocks_* as driven by
  * pipeline.compress / container.encode_stream (pipeline.py:112-191,

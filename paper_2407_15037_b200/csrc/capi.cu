@@ -180,6 +180,14 @@ int gebq_splitmix64_fill(uint64_t *out, int64_t n, uint64_t seed, int64_t start_
 int gebq_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_index, void *stream) {
     return launch_gen_mixed_f32(out, n, seed, start_index, S(stream));
 }
+int gebq_verify_f32(const uint32_t *original, const uint32_t *recon, int64_t n, int rel, float bound,
+                    unsigned long long *out5, uint8_t *mask, void *stream) {
+    return launch_verify<float>(rel, original, recon, n, bound, out5, mask, S(stream));
+}
+int gebq_verify_f64(const uint64_t *original, const uint64_t *recon, int64_t n, int rel, double bound,
+                    unsigned long long *out5, uint8_t *mask, void *stream) {
+    return launch_verify<double>(rel, original, recon, n, bound, out5, mask, S(stream));
+}
 
 }  // extern "C"
 

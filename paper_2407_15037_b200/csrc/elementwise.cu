@@ -472,4 +472,85 @@ int launch_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_
     return check_launch("gen_mixed_f32");
 }
 
+// ---------------------------------------------------------------------------
+// verify (verify.py:88-153): the bound predicates of the compressor's
+// double-check, evaluated on (original, reconstructed) pairs on the device.
+//   out5[0] += violations       (finite original, bits differ, predicate false)
+//   out5[1] += special mismatches (NaN/Inf original, bits differ)
+//   out5[2]  = min index of a violation (caller sets UINT64_MAX)
+//   out5[3]  = max over inexact finite elements of |o - r| (ABS/NOA) or
+//              |q - 1| (REL, q = |r| / |o|) as binary64 bits (NaN -> +inf)
+//   mask (optional): 1 = violation, 2 = special mismatch, 0 otherwise
+// ---------------------------------------------------------------------------
+template <typename T, bool kRel>
+__global__ void __launch_bounds__(kThreads) k_verify(const typename W<T>::U *__restrict__ o,
+                                                     const typename W<T>::U *__restrict__ r, int64_t n,
+                                                     T bound, unsigned long long *out5, uint8_t *mask) {
+    using X = W<T>;
+    using U = typename X::U;
+    unsigned long long viol = 0, spec = 0, first = ~0ull, maxe = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const U ob = o[i], rb = r[i];
+        const bool eq = ob == rb;
+        const bool special = (ob & X::kAbsMask) >= (X::kExpAll << X::kMantBits);
+        uint8_t mk = 0;
+        if (special) {
+            if (!eq) { spec++; mk = 2; }
+        } else if (!eq) {
+            const T of = X::from_bits(ob), rf = X::from_bits(rb);
+            bool ok;
+            double dev;
+            if constexpr (kRel) {
+                const bool same_sign = (ob >> (X::kBits - 1)) == (rb >> (X::kBits - 1));
+                const T q = X::div(X::fabs_(rf), X::fabs_(of));
+                ok = same_sign && q <= bound && X::mul(q, bound) >= T(1);
+                dev = fabs(__dsub_rn((double)q, 1.0));
+            } else {
+                const T err = X::fabs_(X::sub(of, rf));
+                ok = err <= bound;
+                dev = (double)err;
+            }
+            if (dev != dev) dev = __longlong_as_double(0x7FF0000000000000ll);
+            const unsigned long long db = (unsigned long long)__double_as_longlong(dev);
+            maxe = db > maxe ? db : maxe;
+            if (!ok) {
+                viol++;
+                first = (unsigned long long)i < first ? (unsigned long long)i : first;
+                mk = 1;
+            }
+        }
+        if (mask) mask[i] = mk;
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        viol += __shfl_xor_sync(0xFFFFFFFFu, viol, off);
+        spec += __shfl_xor_sync(0xFFFFFFFFu, spec, off);
+        const unsigned long long f2 = __shfl_xor_sync(0xFFFFFFFFu, first, off);
+        first = f2 < first ? f2 : first;
+        const unsigned long long m2 = __shfl_xor_sync(0xFFFFFFFFu, maxe, off);
+        maxe = m2 > maxe ? m2 : maxe;
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (viol) atomicAdd(&out5[0], viol);
+        if (spec) atomicAdd(&out5[1], spec);
+        if (first != ~0ull) atomicMin(&out5[2], first);
+        if (maxe) atomicMax(&out5[3], maxe);
+    }
+}
+
+template <typename T>
+int launch_verify(int rel, const void *o, const void *r, int64_t n, T bound, unsigned long long *out5,
+                  uint8_t *mask, cudaStream_t st) {
+    using U = typename W<T>::U;
+    if (n <= 0) return 0;
+    const int grid = grid_for(n);
+    if (rel) k_verify<T, true><<<grid, kThreads, 0, st>>>((const U *)o, (const U *)r, n, bound, out5, mask);
+    else k_verify<T, false><<<grid, kThreads, 0, st>>>((const U *)o, (const U *)r, n, bound, out5, mask);
+    return check_launch("verify");
+}
+template int launch_verify<float>(int, const void *, const void *, int64_t, float, unsigned long long *, uint8_t *,
+                                  cudaStream_t);
+template int launch_verify<double>(int, const void *, const void *, int64_t, double, unsigned long long *,
+                                   uint8_t *, cudaStream_t);
+
 }  // namespace gebq

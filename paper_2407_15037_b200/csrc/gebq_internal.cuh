@@ -52,6 +52,9 @@ template <typename T>
 int launch_sweep(int mode, int unsafe, int source, uint64_t start, int64_t count, const void *bits,
                  uint64_t seed, const Consts<T> &k, unsigned long long *tally15,
                  unsigned long long *first, cudaStream_t st);
+template <typename T>
+int launch_verify(int rel, const void *o, const void *r, int64_t n, T bound, unsigned long long *out5,
+                  uint8_t *mask, cudaStream_t st);
 int launch_splitmix64_fill(uint64_t *out, int64_t n, uint64_t seed, int64_t start_index,
                            cudaStream_t st);
 int launch_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_index,

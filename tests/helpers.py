@@ -47,3 +47,28 @@ def mixed_bits(width, n, seed):
                              0x7FF8000000000000, 1, 0x7FEFFFFFFFFFFFFF, 0x0010000000000000,
                              0x3FF0000000000000, 0xBFF0000000000000], dtype=np.uint64)
     return np.concatenate([specials, bits])
+
+
+def verify_numpy(o, r, mode, d, value_range=None):
+    """numpy restatement of the reference's verify predicates (verify.py:88-153):
+    returns (violations, first_violation_index, special_mismatch_count, max_err)."""
+    itype = np.uint32 if o.dtype == np.float32 else np.uint64
+    ob, rb = o.view(itype), r.view(itype)
+    eq = ob == rb
+    special = np.isnan(o) | np.isinf(o)
+    spec = int(np.count_nonzero(special & ~eq))
+    inexact = ~special & ~eq
+    with np.errstate(all="ignore"):
+        if mode == "rel":
+            q = np.abs(r) / np.abs(o)
+            ok = (np.signbit(o) == np.signbit(r)) & (q <= d["op_eps"]) & (q * d["op_eps"] >= o.dtype.type(1.0))
+            dev = np.abs(q[inexact].astype(np.float64) - 1.0)
+        else:
+            err = np.abs(o - r)
+            ok = err <= d["eb_eff"]
+            dev = err[inexact].astype(np.float64)
+    mx = float(np.max(np.where(np.isnan(dev), np.inf, dev))) if dev.size else 0.0
+    bad = ~special & ~(eq | ok)
+    viol = int(np.count_nonzero(bad))
+    first = int(np.flatnonzero(bad)[0]) if viol else None
+    return viol, first, spec, mx

@@ -298,3 +298,41 @@ def test_pipelined_compress_vs_oracle(cuda, oracle, mode, eb, bs, pinned, n):
     assert len(s) == len(so)
     assert s == so
     assert trig_list(st.triggers) == list(trig)
+
+
+@pytest.mark.parametrize("width", [32, 64])
+@pytest.mark.parametrize("mode,eb,vr", [("abs", 1e-3, None), ("rel", 1e-2, None), ("noa", 1e-3, 3.0)])
+def test_device_verify_matches_reference_predicates(cuda, oracle, width, mode, eb, vr):
+    """verify() on the device == the reference's numpy predicates, on honest
+    round trips (0 violations) and on corrupted reconstructions."""
+    import paper_2407_15037_b200 as g
+    from helpers import mixed_bits, verify_numpy
+
+    ft = np.float32 if width == 32 else np.float64
+    it = np.uint32 if width == 32 else np.uint64
+    x = mixed_bits(width, 200_003, 5).view(ft)
+    cfg = g.QuantConfig(mode=mode, eb=eb, width=width, value_range=vr)
+    y = g.decompress_to_array(g.compress(x, cfg)[0])
+    d = oracle.derive(mode, eb, width, vr)
+    rep = g.verify(x, y, mode, eb, vr)
+    assert rep.passed and rep.violations == 0
+    assert verify_numpy(x, y, mode, d, vr)[0] == 0
+    rng = np.random.default_rng(3)
+    yb = y.view(it).copy()
+    idx = rng.choice(len(yb), 2000, replace=False)
+    yb[idx] ^= it(1) << rng.integers(0, width, 2000).astype(it)
+    z = yb.view(ft)
+    rep = g.verify(x, z, mode, eb, vr)
+    viol, first, spec, mx = verify_numpy(x, z, mode, d, vr)
+    assert (rep.violations, rep.first_violation_index, rep.special_mismatch_count) == (viol, first, spec)
+    got = rep.max_rel_ratio_deviation if mode == "rel" else rep.max_abs_err
+    assert got == mx
+    assert len(rep.special_mismatches) == spec
+
+
+def test_check_golden_on_gpu(cuda):
+    """The reference's golden record (verify.py:165-272) reproduced by the GPU path."""
+    import paper_2407_15037_b200 as g
+
+    res = g.check_golden()
+    assert res["passed"], res

@@ -138,3 +138,32 @@ def test_no_cpu_fallback_without_gpu():
         g.compress(np.ones(10, np.float32), g.QuantConfig(mode="abs", eb=1e-3))
     with pytest.raises(NoDeviceError):
         g.sweep_f32("abs", [1e-3], count=100)
+
+
+def test_verify_argument_errors_without_gpu():
+    """verify() validates its arguments like the reference (verify.py:95-115)
+    before touching the device."""
+    import paper_2407_15037_b200 as g
+
+    a = np.zeros(4, np.float32)
+    with pytest.raises(g.LengthMismatch):
+        g.verify(a, np.zeros(5, np.float32), "abs", 1e-3)
+    with pytest.raises(g.LengthMismatch):
+        g.verify(a, np.zeros(4, np.float64), "abs", 1e-3)
+    with pytest.raises(g.InvalidBound):
+        g.verify(a, a, "abs", 0.0)
+    with pytest.raises(ValueError):
+        g.verify(a, a, "noa", 1e-3)
+    with pytest.raises(ValueError):
+        g.verify(a, a, "xyz", 1e-3)
+    assert g.verify(np.zeros(0, np.float32), np.zeros(0, np.float32), "rel", 1e-2).passed
+
+
+def test_golden_record_shipped_with_package(golden_record):
+    """The package's golden.json is the reference's record (pinned by the fixtures)."""
+    import importlib
+
+    v = importlib.import_module("paper_2407_15037_b200.verify")
+    rec = v.load_golden_record()
+    assert rec["overall"] == golden_record["overall"]
+    assert rec["overall"].startswith("fe741cd1")
