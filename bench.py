@@ -396,6 +396,8 @@ def main():
     dec_gbs = dec_bytes / (dec_ms * 1e-3) / 1e9
     dominant = ("encode", enc_ms, enc_bytes, enc_gbs) if enc_ms >= dec_ms else ("decode", dec_ms, dec_bytes, dec_gbs)
     traffic = load_traffic(args.workload)
+    if isinstance(traffic, dict):
+        traffic = traffic.get(dominant[0])
 
     # end-to-end through the public API with pinned host buffers
     e2e = None
