@@ -229,11 +229,12 @@ int gebq_decode_rel_f64(const uint8_t *region, int64_t region_len,
                         const long long *region_len_dev, const int64_t *offsets, int64_t nblocks,
                         int64_t count, int64_t block_size, double w, const void *derived_dev,
                         uint64_t *out, unsigned long long *err_key, void *stream);
-/* Self-check of the division-free REL filter inside the f32 stream encoder:
- * for patterns [start, start+count) mod 2^32, out2[0] += values whose
- * certified fast-path (code, trigger) differs from the reference op sequence
- * (quantize_rel32, _kernels.py:165-224) -- must stay 0 -- and out2[1] +=
- * values deferred to the exact sequence.                                    */
+/* Self-check of the production REL binary32 quantizers (the stream
+ * encoder's exact-division one and the CodedArray kernel's division-free
+ * filtered one) against the reference op sequence (quantize_rel32,
+ * _kernels.py:165-224) for patterns [start, start+count) mod 2^32:
+ * out2[0] += mismatching (code, trigger) outcomes -- must stay 0;
+ * out2[1] is unused (0).                                                    */
 int gebq_selfcheck_rel_filter_f32(uint64_t start, int64_t count, float op_eps, float w, float thr,
                                   int unsafe, unsigned long long *out2, void *stream);
 

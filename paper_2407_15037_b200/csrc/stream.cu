@@ -644,7 +644,7 @@ static int64_t blocks_per_tile(int64_t bs) { return bs <= kEncTileMax ? kEncTile
 size_t encode_workspace_bytes(int64_t n, int64_t bs, int width) {
     const int64_t nblocks = n ? (n + bs - 1) / bs : 0;
     if (bs == kEncTileMax) {
-        // specialised path (slots + totals + offsets); also covers the generic one
+        // specialised single-pass path (tile counters); also covers the generic one
         const int64_t V = kEncTileMax;
         const int64_t ntiles = (n + V - 1) / V;
         const size_t gen = (size_t)(ntiles + 2) * 8 + 256;
