@@ -48,7 +48,15 @@ WORKLOADS = {
                eb=1e-3, width=64, n=1 << 28, scaling="weak"),
     "c5rel": dict(desc="C5: REL f64 eb=1e-3, 2^28 random splitmix64 doubles per GPU", mode="rel",
                   eb=1e-3, width=64, n=1 << 28, scaling="weak"),
+    "c4": dict(desc="C4: exhaustive sweep of all 2^32 f32 patterns through ABS 1e-3, REL 1e-2 and "
+                    "NOA 1e-4 (R=1), pattern range sharded over the GPUs", mode="sweep", eb=None,
+               width=32, n=1 << 32, scaling="strong"),
 }
+
+# exhaustive 2^32 tallies (normal class quantized / lossless)
+C4_CONFIGS = (("abs", 1e-3, None, 2443713898, 1817698966),
+              ("rel", 1e-2, None, 3974120554, 287292310),
+              ("noa", 1e-4, 1.0, 2363099024, 1898313840))
 
 
 def parse_args():
@@ -275,12 +283,165 @@ def run_reference(args, wl, name):
 
 
 # ---------------------------------------------------------------------------
+# C4: exhaustive 2^32 sweeps (sweep.py:172-191), both arms
+# ---------------------------------------------------------------------------
+def _expected_tally(mode, q, l):
+    t = np.zeros((5, 3), dtype=np.int64)
+    t[3, 1] = 2                       # +-inf: lossless
+    t[4, 1] = 16777214                # NaN: lossless
+    if mode == "rel":
+        t[0, 1], t[1, 1] = 2, 16777214   # zero / denormal: lossless (REL guard)
+    else:
+        t[0, 0], t[1, 0] = 2, 16777214   # zero / denormal: quantized
+    t[2, 0], t[2, 1] = q, l
+    return t
+
+
+def run_sweep_bench(args, wl):
+    """One step = the three Appendix-B configurations swept over this rank's
+    share of the 2^32 patterns (generated in-kernel: no HBM input).  value =
+    3 x 2^32 x 4 B / step time (input-bytes convention), plus patterns/s."""
+    world, rank, local = dist_env()
+    total = 1 << 32
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        from oracle import oracle as orc
+
+        orc.lib()
+        cores = os.cpu_count() or 1
+        sample = 1 << 27                      # per config, a bounded slice of the range
+        start = 0x3F000000
+        for _ in range(max(args.warmup, 1)):
+            orc.sweep_f32_range("abs", 1e-3, start, 1 << 22, workers=cores)
+        times = []
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            for mode, eb, vr, _q, _l in C4_CONFIGS:
+                orc.sweep_f32_range(mode, eb, start, sample, value_range=vr, workers=cores)
+            times.append(time.perf_counter() - t0)
+        t = float(np.mean(times))
+        pps = 3 * sample / t
+        value = pps * 4 / 1e9
+        line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (all f32 bit patterns)",
+                "config": {"workload": wl["desc"], "sample": f"3 x 2^27 patterns from 0x3F000000 per step"},
+                "patterns_per_s": pps,
+                "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port",
+                                 "sample": "3 configs x 2^27 consecutive patterns per step"},
+                "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2407_15037_b200 import _lib, device as gdev
+    from paper_2407_15037_b200.quantizers import QuantConfig
+    from paper_2407_15037_b200.sweep import sweep_f32
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.load()
+    per = total // world
+    start = rank * per
+    count = total - start if rank == world - 1 else per
+    cfgs = [QuantConfig(mode=m, eb=eb, width=32, value_range=vr) for m, eb, vr, _q, _l in C4_CONFIGS]
+    tallies = [torch.zeros(15, dtype=torch.int64, device=dev) for _ in cfgs]
+    firsts = [torch.full((1,), -1, dtype=torch.int64, device=dev) for _ in cfgs]
+    st = torch.cuda.current_stream()
+
+    def step(acc):
+        for c, t, f in zip(cfgs, tallies, firsts):
+            if not acc:
+                t.zero_()
+                f.fill_(-1)
+            gdev.sweep(c, source=gdev.SOURCE_RANGE, start=start, count=count, tally=t, first=f)
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    # correctness of the last sweep against SURVEY Appendix B (summed over ranks)
+    tl = torch.stack(tallies)
+    if world > 1:
+        dist.all_reduce(tl)
+    tl = tl.cpu().numpy().reshape(3, 5, 3)
+    match = all(np.array_equal(tl[i], _expected_tally(m, q, l)) for i, (m, _e, _v, q, l) in enumerate(C4_CONFIGS))
+    violations = int(tl[:, :, 2].sum())
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0e = torch.cuda.Event(enable_timing=True)
+    t1e = torch.cuda.Event(enable_timing=True)
+    launches0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        t0e.record(st)
+        for _ in range(args.steps):
+            step(False)
+        t1e.record(st)
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    ms = torch.tensor([t0e.elapsed_time(t1e) / args.steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    pps = 3 * total / (ms * 1e-3)
+    value = pps * 4 / 1e9
+    # e2e: the public API (sweep_f32 -> SweepReport on the host), this rank's share
+    t0 = time.perf_counter()
+    for m, eb, vr, _q, _l in C4_CONFIGS:
+        sweep_f32(m, [eb], value_range=vr, start=start, count=count)
+    torch.cuda.synchronize()
+    el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    e2e = 3 * total * 4 / float(el.item()) / 1e9
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as orc
+
+        orc.lib()
+        cores = os.cpu_count() or 1
+        sample = 1 << 27
+        t0 = time.perf_counter()
+        for mth, eb, vr, _q, _l in C4_CONFIGS:
+            orc.sweep_f32_range(mth, eb, 0x3F000000, sample, value_range=vr, workers=cores)
+        tc = time.perf_counter() - t0
+        cpu = {"value": 3 * sample * 4 / tc / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
+               "sample": f"3 configs x 2^27 patterns from 0x3F000000 ({tc:.1f} s) on {cores} threads"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (all 2^32 f32 bit patterns, generated in-kernel)",
+                "config": {"workload": wl["desc"], "patterns_per_gpu": count,
+                           "parallelism": f"dp{world} (contiguous pattern ranges)",
+                           "gbs_basis": "4 B per pattern x 3 configurations per step"},
+                "patterns_per_s": pps, "violations": violations, "tallies_match_appendix_b": bool(match),
+                "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 3 * 16 * 8,
+                        "api": "paper_2407_15037_b200.sweep_f32 (SweepReport to the host)"},
+                "roofline": {"bound": "alu", "achieved": None, "peak": None, "unit": None, "frac": None,
+                             "traffic": None, "note": "no HBM input: patterns are generated in-kernel"},
+                "cpu_baseline": cpu, "clocks": clk.summary(), "gpu_launches": launches}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+# ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
 def main():
     args = parse_args()
     args.warmup = max(args.warmup, 3)
     wl = WORKLOADS[args.workload]
+    if args.workload == "c4":
+        return run_sweep_bench(args, wl)
     if args.impl == "reference":
         return run_reference(args, wl, args.workload)
 
