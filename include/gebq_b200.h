@@ -136,6 +136,16 @@ int gebq_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_in
                        void *stream);
 
 
+/* ---- library-log REL variant: quantize_rel32_lib / reconstruct_rel32_lib
+ * (_kernels.py:356-431).  Non-conforming by design (binary64 library
+ * log2/exp2 instead of the bit-level approximations; GPU and host libm may
+ * differ in the last ulp), bound still guaranteed by the double-check.
+ * Benchmark comparisons only (bench.py:143-201 "library_log").              */
+int gebq_quantize_rel_lib_f32(const uint32_t *x, uint32_t *codes, uint8_t *lossless, int64_t n, float op_eps,
+                              float w, float thr, int unsafe, unsigned long long *trig4, void *stream);
+int gebq_dequantize_rel_lib_f32(const uint32_t *codes, const uint8_t *lossless, uint32_t *out, int64_t n, float w,
+                                void *stream);
+
 /* ---- verify: verify.py:88-153 on the device -------------------------------
  * rel = 1: bound = op_eps (same sign, q = |r|/|o|, q <= op_eps, q*op_eps >= 1);
  * rel = 0: bound = eb_eff (|o - r| <= eb_eff; ABS and NOA).  NaN/Inf

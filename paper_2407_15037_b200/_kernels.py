@@ -32,7 +32,8 @@ __all__ = [
     "reconstruct_abs32", "reconstruct_abs64", "reconstruct_rel32", "reconstruct_rel64",
     "block_sizes_u32", "block_sizes_u64", "emit_blocks_u32", "emit_blocks_u64",
     "decode_blocks_u32", "decode_blocks_u64", "sweep_abs32_on", "sweep_abs64_on",
-    "sweep_rel32_on", "sweep_rel64_on", "splitmix64_fill", "MAXBIN32", "MAXBIN64",
+    "sweep_rel32_on", "sweep_rel64_on", "splitmix64_fill", "quantize_rel32_lib",
+    "reconstruct_rel32_lib", "MAXBIN32", "MAXBIN64",
 ]
 
 
@@ -105,6 +106,36 @@ def reconstruct_rel32(codes, lossless, out_bits, out_vals, w):
 
 def reconstruct_rel64(codes, lossless, out_bits, out_vals, w):
     return _reconstruct(codes, lossless, out_bits, "rel", np.float64(w))
+
+
+# ---- library-log REL variant (_kernels.py:356-431; non-conforming by design) --
+def quantize_rel32_lib(bits, vals, codes, lossless, op_eps, w, thr, unsafe):
+    n = len(bits)
+    if n == 0:
+        return np.zeros(4, dtype=np.int64)
+    x = device.to_device(np.ascontiguousarray(bits))
+    c = torch.empty_like(x)
+    ll = torch.empty(n, dtype=torch.uint8, device=x.device)
+    trig = torch.zeros(4, dtype=torch.int64, device=x.device)
+    _lib.call("gebq_quantize_rel_lib_f32", device._p(x), device._p(c), device._p(ll), n,
+              np.float32(op_eps).item(), np.float32(w).item(), np.float32(thr).item(), int(bool(unsafe)),
+              device._p(trig), device._s())
+    codes[...] = c.cpu().numpy().view(codes.dtype)
+    lossless[...] = ll.cpu().numpy().view(np.bool_)
+    return trig.cpu().numpy().astype(np.int64)
+
+
+def reconstruct_rel32_lib(codes, lossless, out_bits, out_vals, w):
+    n = len(codes)
+    if n == 0:
+        return 0
+    c = device.to_device(np.ascontiguousarray(codes))
+    ll = device.to_device(np.ascontiguousarray(lossless, dtype=np.bool_))
+    out = torch.empty_like(c)
+    _lib.call("gebq_dequantize_rel_lib_f32", device._p(c), device._p(ll), device._p(out), n,
+              np.float32(w).item(), device._s())
+    out_bits[...] = out.cpu().numpy().view(out_bits.dtype)
+    return 0
 
 
 # ---- block payload (_kernels.py:606-664) --------------------------------------

@@ -51,6 +51,8 @@ SIGNATURES = {
     "gebq_sweep_rel_f64": [_int, _vp, _u64, _i64, _u64, _f64, _f64, _f64, _int, _vp, _vp, _vp],
     "gebq_splitmix64_fill": [_vp, _i64, _u64, _i64, _vp],
     "gebq_gen_mixed_f32": [_vp, _i64, _u64, _i64, _vp],
+    "gebq_quantize_rel_lib_f32": [_vp, _vp, _vp, _i64, _f32, _f32, _f32, _int, _vp, _vp],
+    "gebq_dequantize_rel_lib_f32": [_vp, _vp, _vp, _i64, _f32, _vp],
     "gebq_verify_f32": [_vp, _vp, _i64, _int, _f32, _vp, _vp, _vp],
     "gebq_verify_f64": [_vp, _vp, _i64, _int, _f64, _vp, _vp, _vp],
     "gebq_encode_region_capacity": [_i64, _i64, _int],

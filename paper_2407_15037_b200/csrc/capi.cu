@@ -180,6 +180,14 @@ int gebq_splitmix64_fill(uint64_t *out, int64_t n, uint64_t seed, int64_t start_
 int gebq_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_index, void *stream) {
     return launch_gen_mixed_f32(out, n, seed, start_index, S(stream));
 }
+int gebq_quantize_rel_lib_f32(const uint32_t *x, uint32_t *codes, uint8_t *lossless, int64_t n, float op_eps,
+                              float w, float thr, int unsafe, unsigned long long *trig4, void *stream) {
+    return launch_rel32_lib_quantize(x, codes, lossless, n, op_eps, w, thr, unsafe, trig4, S(stream));
+}
+int gebq_dequantize_rel_lib_f32(const uint32_t *codes, const uint8_t *lossless, uint32_t *out, int64_t n, float w,
+                                void *stream) {
+    return launch_rel32_lib_reconstruct(codes, lossless, out, n, w, S(stream));
+}
 int gebq_verify_f32(const uint32_t *original, const uint32_t *recon, int64_t n, int rel, float bound,
                     unsigned long long *out5, uint8_t *mask, void *stream) {
     return launch_verify<float>(rel, original, recon, n, bound, out5, mask, S(stream));

@@ -473,6 +473,83 @@ int launch_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_
 }
 
 // ---------------------------------------------------------------------------
+// library-log REL variant (quantize_rel32_lib / reconstruct_rel32_lib,
+// _kernels.py:356-431): the same guard chain and double-check, but log2 / 2^p
+// from the binary64 math library instead of the bit-level approximations.
+// Non-conforming by design (the reference says so): CUDA's log2/exp2 are not
+// the host libm, so codes may differ from the CPU in rare last-ulp cases; the
+// double-check still guarantees the bound.  Benchmark comparisons only.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_quantize_rel32_lib(const uint32_t *__restrict__ x, uint32_t *codes,
+                                                                 uint8_t *flags, int64_t n, float op_eps, float w,
+                                                                 float thr, int unsafe, unsigned long long *trig) {
+    uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t xb = x[i];
+        const float xf = __uint_as_float(xb);
+        int tr = TRIG_NONE;
+        uint32_t code = xb;
+        const uint32_t ab = xb & 0x7FFFFFFFu;
+        const uint32_t aexpo = ab >> 23;
+        if (xf != xf) tr = TRIG_NAN;
+        else if (aexpo == 0xFFu) tr = TRIG_INF;
+        else if (aexpo == 0) tr = TRIG_GUARD;
+        else {
+            const float l = __double2float_rn(log2((double)fabsf(xf)));
+            const float t = __fdiv_rn(l, w);
+            if (!(fabsf(t) < thr)) tr = TRIG_GUARD;
+            else {
+                float kf;
+                const int32_t kb = round_bin(t, kf);
+                if (kb >= (1 << 30) || kb <= -(1 << 30)) tr = TRIG_GUARD;
+                else {
+                    const float p = __fmul_rn(kf, w);
+                    if (!(p > -127.0f && p < 128.0f)) tr = TRIG_GUARD;
+                    else {
+                        if (!unsafe) {
+                            const float recon = __double2float_rn(exp2((double)p));
+                            const float q = __fdiv_rn(recon, fabsf(xf));
+                            if (!(q <= op_eps && __fmul_rn(q, op_eps) >= 1.0f)) tr = TRIG_DCHECK;
+                        }
+                        if (tr == TRIG_NONE) code = (zigzag_w(kb) << 1) | (xb >> 31);
+                    }
+                }
+            }
+        }
+        codes[i] = code;
+        flags[i] = tr != TRIG_NONE;
+        c0 += tr == TRIG_NAN; c1 += tr == TRIG_INF; c2 += tr == TRIG_GUARD; c3 += tr == TRIG_DCHECK;
+    }
+    flush_trig(c0, c1, c2, c3, trig);
+}
+
+__global__ void __launch_bounds__(kThreads) k_reconstruct_rel32_lib(const uint32_t *__restrict__ codes,
+                                                                    const uint8_t *__restrict__ flags, uint32_t *out,
+                                                                    int64_t n, float w) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = codes[i];
+        if (flags[i]) { out[i] = c; continue; }
+        const int32_t kb = unzigzag_w(c >> 1);
+        const float p = __fmul_rn(__int2float_rn(kb), w);
+        const float mag = __double2float_rn(exp2((double)p));
+        out[i] = __float_as_uint(mag) | (c << 31);
+    }
+}
+
+int launch_rel32_lib_quantize(const uint32_t *x, uint32_t *codes, uint8_t *flags, int64_t n, float op_eps, float w,
+                              float thr, int unsafe, unsigned long long *trig, cudaStream_t st) {
+    if (n <= 0) return 0;
+    k_quantize_rel32_lib<<<grid_for(n), kThreads, 0, st>>>(x, codes, flags, n, op_eps, w, thr, unsafe, trig);
+    return check_launch("quantize_rel32_lib");
+}
+int launch_rel32_lib_reconstruct(const uint32_t *codes, const uint8_t *flags, uint32_t *out, int64_t n, float w,
+                                 cudaStream_t st) {
+    if (n <= 0) return 0;
+    k_reconstruct_rel32_lib<<<grid_for(n), kThreads, 0, st>>>(codes, flags, out, n, w);
+    return check_launch("reconstruct_rel32_lib");
+}
+
+// ---------------------------------------------------------------------------
 // verify (verify.py:88-153): the bound predicates of the compressor's
 // double-check, evaluated on (original, reconstructed) pairs on the device.
 //   out5[0] += violations       (finite original, bits differ, predicate false)

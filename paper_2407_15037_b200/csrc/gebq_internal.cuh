@@ -55,6 +55,10 @@ int launch_sweep(int mode, int unsafe, int source, uint64_t start, int64_t count
 template <typename T>
 int launch_verify(int rel, const void *o, const void *r, int64_t n, T bound, unsigned long long *out5,
                   uint8_t *mask, cudaStream_t st);
+int launch_rel32_lib_quantize(const uint32_t *x, uint32_t *codes, uint8_t *flags, int64_t n, float op_eps, float w,
+                              float thr, int unsafe, unsigned long long *trig, cudaStream_t st);
+int launch_rel32_lib_reconstruct(const uint32_t *codes, const uint8_t *flags, uint32_t *out, int64_t n, float w,
+                                 cudaStream_t st);
 int launch_splitmix64_fill(uint64_t *out, int64_t n, uint64_t seed, int64_t start_index,
                            cudaStream_t st);
 int launch_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_index,

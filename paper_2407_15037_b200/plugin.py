@@ -22,7 +22,8 @@ KERNEL_NAMES = (
     "reconstruct_abs32", "reconstruct_abs64", "reconstruct_rel32", "reconstruct_rel64",
     "block_sizes_u32", "block_sizes_u64", "emit_blocks_u32", "emit_blocks_u64",
     "decode_blocks_u32", "decode_blocks_u64", "sweep_abs32_on", "sweep_abs64_on",
-    "sweep_rel32_on", "sweep_rel64_on", "splitmix64_fill",
+    "sweep_rel32_on", "sweep_rel64_on", "splitmix64_fill", "quantize_rel32_lib",
+    "reconstruct_rel32_lib",
 )
 
 

@@ -193,3 +193,34 @@ def test_generators(cuda):
     np.testing.assert_array_equal(a, workloads.splitmix64(100003, 0x9E3779B97F4A7C15, 7))
     b = device.mixed_f32(1 << 20, workloads.C2_SEED).cpu().numpy().view(np.uint32)
     np.testing.assert_array_equal(b, workloads.c2_values(1 << 20).view(np.uint32))
+
+
+@pytest.mark.parametrize("eb", [1e-2, 1e-3])
+def test_library_log_variant(cuda, eb):
+    """quantize_rel32_lib / reconstruct_rel32_lib (_kernels.py:356-431) against the
+    reference's own outputs (tests/golden/lib_variant.npz).  The variant uses the
+    platform binary64 log2/exp2 and is non-conforming by design, so: the bound
+    holds for every value, and codes / reconstructions agree with the CPU
+    reference except for rare last-ulp libm differences."""
+    import os
+
+    import paper_2407_15037_b200 as g
+    from paper_2407_15037_b200 import _kernels as K
+    from paper_2407_15037_b200.quantizers import QuantConfig
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "lib_variant.npz"))
+    bits = z["x"]
+    x = bits.view(np.float32)
+    tag = f"{eb:g}"
+    d = QuantConfig(mode="rel", eb=eb, width=32).derived
+    codes = np.empty(len(bits), np.uint32)
+    ll = np.empty(len(bits), np.bool_)
+    trig = K.quantize_rel32_lib(bits, x, codes, ll, d.op_eps, d.w, d.thr, False)
+    rec = np.empty(len(bits), np.float32)
+    K.reconstruct_rel32_lib(codes, ll, rec.view(np.uint32), rec, d.w)
+    rep = g.verify(x, rec, "rel", eb)
+    assert rep.passed, rep.summary()
+    agree = np.mean((codes == z[f"codes_{tag}"]) & (ll == z[f"lossless_{tag}"]))
+    assert agree > 0.999, agree
+    assert np.mean(rec.view(np.uint32) == z[f"recon_{tag}"]) > 0.999
+    assert abs(int(trig.sum()) - int(z[f"trig_{tag}"].sum())) <= len(bits) // 1000
