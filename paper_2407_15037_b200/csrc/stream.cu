@@ -724,7 +724,12 @@ int launch_encode(const EncodeCfg &cfg, const void *x, const uint8_t *flags_in, 
         return cfg.unsafe ? GEN(0, MODE_ABS, true) : GEN(0, MODE_ABS, false);
 #undef GEN
     }
-    if (cfg.block_size == kEncTileMax && cfg.src == 0 && !force_generic_kernels())
+    // the specialised REL binary32 encoder divides by w through a hoisted refined
+    // reciprocal, exact for w in [2^-100, 2^100]; other (degenerate) bounds take
+    // the generic kernel with plain IEEE division
+    const bool w_ok = !(cfg.mode == MODE_REL && sizeof(T) == 4) ||
+                      ((double)k.b >= 0x1p-100 && (double)k.b <= 0x1p100);
+    if (cfg.block_size == kEncTileMax && cfg.src == 0 && w_ok && !force_generic_kernels())
         return launch_encode4k<T>(cfg, x, k, kdev, region, index, ws, trig, region_len, st);
     EncArgs<T> a;
     a.x = xp;
