@@ -11,7 +11,8 @@ import ctypes
 import os
 import threading
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libgebq_b200.so")
+LIB_PATH = os.environ.get("GEBQ_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                            "libgebq_b200.so")
 
 
 class GebqCudaError(RuntimeError):
