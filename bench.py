@@ -560,6 +560,50 @@ def main():
     if isinstance(traffic, dict):
         traffic = traffic.get(dominant[0])
 
+    # the CodedArray stage alone (quantize_* -> codes + flags, reconstruct_*), the
+    # reference's quantizer boundary before the lossless container: not part of
+    # the step, reported beside it (same batch, device resident)
+    coded = None
+    if not os.environ.get("GEBQ_B200_NO_CODED"):
+        consts_c = None
+        if wl["mode"] == NOA:
+            consts_c, _ = gdev.noa_derive(keys, wl["eb"], wl["width"])
+        codes_c = torch.empty_like(x)
+        ll_c = torch.empty(n, dtype=torch.uint8, device=dev)
+        trig_c = torch.zeros(4, dtype=torch.int64, device=dev)
+        out_c = torch.empty_like(x)
+        rmode = "abs" if wl["mode"] == NOA else wl["mode"]
+        derived_c = None if consts_c is not None else cfg.derived.derived_value
+
+        def coded_step(evq=None):
+            if evq is not None:
+                evq[0].record(st)
+            gdev.quantize(x, cfg, codes=codes_c, lossless=ll_c, trig=trig_c, consts_dev=consts_c)
+            if evq is not None:
+                evq[1].record(st)
+            dv = derived_c if derived_c is not None else float(consts_c[1].item())
+            gdev.reconstruct(codes_c, ll_c, rmode, dv, out=out_c)
+            if evq is not None:
+                evq[2].record(st)
+
+        if consts_c is not None:
+            derived_c = float(consts_c[1].item())
+        for _ in range(3):
+            coded_step()
+        torch.cuda.synchronize()
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+        for i in range(args.steps):
+            coded_step(evs[i])
+        torch.cuda.synchronize()
+        q_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
+        r_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
+        cb = n * (2 * W + 1)
+        coded = {"quantize": {"ms": q_ms, "gbs": cb / (q_ms * 1e-3) / 1e9, "frac": cb / (q_ms * 1e-3) / 1e9 / load_peaks()[0],
+                              "bytes": cb, "basis": "n x (W read + W code + 1 flag)"},
+                 "reconstruct": {"ms": r_ms, "gbs": cb / (r_ms * 1e-3) / 1e9, "frac": cb / (r_ms * 1e-3) / 1e9 / load_peaks()[0],
+                                 "bytes": cb, "basis": "n x (W code + 1 flag read + W value)"},
+                 "value_gbs": 2 * n_all * W / ((q_ms + r_ms) * 1e-3) / 1e9}
+
     # end-to-end through the public API with pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -625,6 +669,7 @@ def main():
                                    "bytes": enc_bytes, "input_gbs": n * W / (enc_ms * 1e-3) / 1e9},
                         "decode": {"ms": dec_ms, "gbs": dec_gbs, "frac": dec_gbs / peak,
                                    "bytes": dec_bytes, "input_gbs": n * W / (dec_ms * 1e-3) / 1e9}},
+            "coded_stage": coded,
             "stream_bytes_per_value": stream_bytes / n, "triggers": trig_h,
             "violations": violations,
             "violations_check": "device verify (verify.py:88-153 predicates) of every decoded value, all ranks",

@@ -69,7 +69,19 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename W<T>::U *_
     using U = typename W<T>::U;
     if (kdev) k = *kdev;  // NOA: constants derived on device from the global range
     RelFast<T> f{};
-    if constexpr (kMode == MODE_REL) f = make_rel_fast<T>(k);
+    RelExact ef{};
+    if constexpr (kMode == MODE_REL) {
+        f = make_rel_fast<T>(k);
+        if constexpr (sizeof(T) == 4) ef = make_rel_exact(k);
+    }
+    // binary32 REL: the exact-division quantizer of the stream encoder whenever w
+    // is in its range (uniform); the filtered one otherwise
+    auto qv = [&](typename W<T>::U xb, typename W<T>::U &c) -> int {
+        if constexpr (kMode == MODE_REL && sizeof(T) == 4) {
+            if (ef.wdiv) return quantize_rel_exact32<kUnsafe>(xb, k, ef, c);
+        }
+        return quantize_bf<T, kMode, kUnsafe>(xb, k, f, c);
+    };
     uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
     auto count = [&](int tr) {
         c0 += tr == TRIG_NAN; c1 += tr == TRIG_INF; c2 += tr == TRIG_GUARD; c3 += tr == TRIG_DCHECK;
@@ -87,7 +99,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename W<T>::U *_
 #pragma unroll
             for (int s = 0; s < 4; s++) {
                 U c;
-                int tr = quantize_bf<T, kMode, kUnsafe>(v[r][s], k, f, c);
+                int tr = qv(v[r][s], c);
                 v[r][s] = c;
                 fl |= (uint32_t)(tr != TRIG_NONE) << (8 * s);
                 count(tr);
@@ -101,7 +113,7 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename W<T>::U *_
     for (int64_t i = start + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         U c;
-        int tr = quantize_bf<T, kMode, kUnsafe>(x[i], k, f, c);
+        int tr = qv(x[i], c);
         codes[i] = c;
         flags[i] = tr != TRIG_NONE;
         count(tr);
