@@ -105,8 +105,8 @@ def encode(x: torch.Tensor, cfg: QuantConfig, *, consts_dev: Optional[torch.Tens
                    trig=trig)
 
 
-COMPRESS_CHUNK = 16 << 20   # input bytes per pipelined span (whole blocks)
-D2H_SLOT = 16 << 20
+COMPRESS_CHUNK = 32 << 20   # input bytes per pipelined span (whole blocks)
+D2H_SLOT = 32 << 20
 
 
 def _encode_span(xb: torch.Tensor, cfg: QuantConfig, region_ptr: int, index_ptr: int,
@@ -425,7 +425,7 @@ def decode_coded_host(data, header: StreamHeader, nblocks: int, index_pos: int):
             lossless.cpu().numpy().view(np.bool_))
 
 
-DECODE_CHUNK = 16 << 20   # stream bytes per pipelined span
+DECODE_CHUNK = 8 << 20    # stream bytes per pipelined span
 
 
 def decode_values_host(data, header: StreamHeader, nblocks: int, index_pos: int) -> np.ndarray:

@@ -278,7 +278,7 @@ def test_rel_filter_exhaustive(cuda, eb, unsafe):
     ("rel", 1e-2, 1000, False, 5 * (1 << 22) + 3),
     ("rel", 1e-3, 4096, True, 1 << 24),
 ])
-def test_pipelined_compress_vs_oracle(cuda, oracle, mode, eb, bs, pinned, n):
+def test_pipelined_compress_vs_oracle(cuda, oracle, mode, eb, bs, pinned, n, monkeypatch):
     """Large inputs take the span-pipelined compress (PCIe overlapped with the
     encode); the bytes must equal the one-shot oracle stream exactly."""
     import torch
@@ -287,6 +287,7 @@ def test_pipelined_compress_vs_oracle(cuda, oracle, mode, eb, bs, pinned, n):
     from paper_2407_15037_b200 import stream, workloads
     from paper_2407_15037_b200.quantizers import QuantConfig
 
+    monkeypatch.setattr(stream, "COMPRESS_CHUNK", 4 << 20)   # many spans, ragged last one
     x = workloads.c2_values(n)
     assert x.nbytes > 2 * stream.COMPRESS_CHUNK
     if pinned:
