@@ -360,3 +360,41 @@ def test_encoder_image_sizes_vs_oracle(cuda, oracle, kind):
         so, trig, _ = oracle.compress(x, mode, eb, workers=8)
         assert s == so, (kind, mode)
         assert trig_list(st.triggers) == list(trig)
+
+
+@pytest.mark.parametrize("width,mode", [(32, "rel"), (32, "abs"), (64, "abs")])
+def test_decode_fuzz_multiblock_vs_oracle(cuda, oracle, width, mode):
+    """Byte mutations of 33-block streams (whole-block bulk copies, edge blocks,
+    the sequential restatement for malformed blocks): same outcome -- error
+    class and byte position, or identical values -- as the oracle."""
+    import re
+
+    import paper_2407_15037_b200 as g
+
+    x = mixed_bits(width, 32 * 4096 + 1000, 21).view(np.float32 if width == 32 else np.float64)
+    base, _ = g.compress(x, _cfg(mode, 1e-2 if mode == "rel" else 1e-3, width))
+    nb = 33
+    region0 = 56 + 8 * nb
+    rng = np.random.default_rng(5)
+
+    def ours(data):
+        try:
+            return "OK:" + sha(g.decompress_to_array(data).tobytes())[:16]
+        except g.ContainerError as e:
+            m = re.search(r"byte (\d+)", str(e))
+            return type(e).__name__ + (":" + m.group(1) if m else "")
+
+    def ref(data):
+        try:
+            return "OK:" + sha(oracle.decompress_to_array(data).tobytes())[:16]
+        except oracle.DecodeError as e:
+            m = re.search(r"byte (\d+)", str(e))
+            return e.kind + (":" + m.group(1) if m else "")
+
+    for t in range(300):
+        s = bytearray(base)
+        for _ in range(int(rng.integers(1, 4))):
+            p = int(rng.integers(region0 if t % 4 else 56, len(s)))
+            s[p] ^= int(rng.integers(1, 256))
+        s = bytes(s)
+        assert ours(s) == ref(s), t
