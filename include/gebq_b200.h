@@ -245,6 +245,10 @@ int gebq_decode_rel_f64(const uint8_t *region, int64_t region_len,
  * _kernels.py:165-224) for patterns [start, start+count) mod 2^32:
  * out2[0] += mismatching (code, trigger) outcomes -- must stay 0;
  * out2[1] is unused (0).                                                    */
+/* Same for the production ABS/NOA binary32 quantizer (quantize_abs32,
+ * _kernels.py:86-123): out2[0] += mismatching outcomes over the range.      */
+int gebq_selfcheck_abs_f32(uint64_t start, int64_t count, float eb_eff, float eb2, float inv_eb2, float thr,
+                           int unsafe, unsigned long long *out2, void *stream);
 int gebq_selfcheck_rel_filter_f32(uint64_t start, int64_t count, float op_eps, float w, float thr,
                                   int unsafe, unsigned long long *out2, void *stream);
 

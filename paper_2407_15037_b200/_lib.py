@@ -81,6 +81,7 @@ SIGNATURES = {
     "gebq_decode_span_abs_f64": [_vp, _i64, _vp, _i64, _i64, _i64, _f64, _i64, _i64, _vp, _vp, _vp],
     "gebq_decode_span_rel_f32": [_vp, _i64, _vp, _i64, _i64, _i64, _f32, _i64, _i64, _vp, _vp, _vp],
     "gebq_decode_span_rel_f64": [_vp, _i64, _vp, _i64, _i64, _i64, _f64, _i64, _i64, _vp, _vp, _vp],
+    "gebq_selfcheck_abs_f32": [_u64, _i64, _f32, _f32, _f32, _f32, _int, _vp, _vp],
     "gebq_selfcheck_rel_filter_f32": [_u64, _i64, _f32, _f32, _f32, _int, _vp, _vp],
     "gebq_decode_blocks_u32": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp],
     "gebq_decode_blocks_u64": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp],

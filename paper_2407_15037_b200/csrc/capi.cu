@@ -350,6 +350,11 @@ int gebq_decode_span_rel_f64(const uint8_t *region, int64_t region_len, const in
 }
 #undef SPAN_CFG
 
+int gebq_selfcheck_abs_f32(uint64_t start, int64_t count, float eb_eff, float eb2, float inv_eb2, float thr,
+                           int unsafe, unsigned long long *out2, void *stream) {
+    Consts<float> k{eb_eff, eb2, inv_eb2, thr};
+    return launch_check_abs_bf(start, count, k, unsafe, out2, S(stream));
+}
 int gebq_selfcheck_rel_filter_f32(uint64_t start, int64_t count, float op_eps, float w, float thr,
                                   int unsafe, unsigned long long *out2, void *stream) {
     Consts<float> k{op_eps, w, 0.0f, thr};

@@ -398,3 +398,25 @@ def test_decode_fuzz_multiblock_vs_oracle(cuda, oracle, width, mode):
             s[p] ^= int(rng.integers(1, 256))
         s = bytes(s)
         assert ours(s) == ref(s), t
+
+
+@pytest.mark.parametrize("eb,vr", [(1e-1, None), (1e-3, None), (1e-5, None), (1e-4, 1.0), (1e-3, 1e10)])
+@pytest.mark.parametrize("unsafe", [False, True])
+def test_abs_quantizer_exhaustive(cuda, eb, vr, unsafe):
+    """Every f32 pattern: the production ABS/NOA quantizer (round-half-even bin
+    via one FRND) gives the reference op sequence's code and trigger."""
+    import ctypes
+
+    import torch
+
+    from paper_2407_15037_b200 import _lib
+    from paper_2407_15037_b200.quantizers import QuantConfig
+
+    mode = "noa" if vr is not None else "abs"
+    d = QuantConfig(mode=mode, eb=eb, width=32, value_range=vr, unsafe_no_double_check=unsafe).derived
+    out = torch.zeros(2, dtype=torch.int64, device="cuda")
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    F = ctypes.c_float
+    _lib.call("gebq_selfcheck_abs_f32", 0, 1 << 32, F(d.eb_eff), F(d.eb2), F(d.inv_eb2), F(d.thr),
+              int(unsafe), ctypes.c_void_p(out.data_ptr()), s)
+    assert out.cpu().tolist()[0] == 0
