@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes
 import os
 import struct
+import threading
 from dataclasses import dataclass
 from typing import Optional
 
@@ -233,15 +234,16 @@ def compress_pipelined(arr: np.ndarray, cfg: QuantConfig, header: StreamHeader):
     return out.finish(hdr_len + total), trig_h
 
 
-_RINGS: dict = {}
+_LOCAL = threading.local()   # per-thread staging rings / streams (concurrent callers never share)
 
 
 def _d2h_ring(dev):
     k = dev.index if dev.index is not None else torch.cuda.current_device()
-    if k not in _RINGS:
-        _RINGS[k] = ([torch.empty(D2H_SLOT, dtype=torch.uint8, pin_memory=True) for _ in range(2)],
-                     [torch.cuda.Event() for _ in range(2)])
-    return _RINGS[k]
+    rings = _LOCAL.__dict__.setdefault("rings", {})
+    if k not in rings:
+        rings[k] = ([torch.empty(D2H_SLOT, dtype=torch.uint8, pin_memory=True) for _ in range(2)],
+                    [torch.cuda.Event() for _ in range(2)])
+    return rings[k]
 
 
 def _d2h_ring_copy(ring, stream, after: torch.cuda.Event, src: torch.Tensor, dst: torch.Tensor, state):
@@ -486,11 +488,9 @@ def decode_values_host(data, header: StreamHeader, nblocks: int, index_pos: int)
     return host.numpy().view(ft)
 
 
-_OUT_STREAMS: dict = {}
-
-
 def _out_stream(dev) -> torch.cuda.Stream:
     k = dev.index if dev.index is not None else torch.cuda.current_device()
-    if k not in _OUT_STREAMS:
-        _OUT_STREAMS[k] = torch.cuda.Stream(device=dev)
-    return _OUT_STREAMS[k]
+    streams = _LOCAL.__dict__.setdefault("out_streams", {})
+    if k not in streams:
+        streams[k] = torch.cuda.Stream(device=dev)
+    return streams[k]

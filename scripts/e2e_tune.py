@@ -27,9 +27,9 @@ for cc in (8 << 20, 16 << 20, 32 << 20):
     for ds in (8 << 20, 16 << 20, 32 << 20):
         stream.COMPRESS_CHUNK = cc
         stream.D2H_SLOT = ds
-        stream._RINGS.clear()
+        stream._LOCAL.__dict__.pop("rings", None)
         run(f"compress chunk {cc>>20}MB d2h slot {ds>>20}MB")
-stream.COMPRESS_CHUNK = 16 << 20; stream.D2H_SLOT = 16 << 20; stream._RINGS.clear()
+stream.COMPRESS_CHUNK = 16 << 20; stream.D2H_SLOT = 16 << 20; stream._LOCAL.__dict__.pop("rings", None)
 for dc in (8 << 20, 16 << 20, 32 << 20, 64 << 20):
     for sl in (8 << 20, 16 << 20, 32 << 20):
         stream.DECODE_CHUNK = dc

@@ -420,3 +420,28 @@ def test_abs_quantizer_exhaustive(cuda, eb, vr, unsafe):
     _lib.call("gebq_selfcheck_abs_f32", 0, 1 << 32, F(d.eb_eff), F(d.eb2), F(d.inv_eb2), F(d.thr),
               int(unsafe), ctypes.c_void_p(out.data_ptr()), s)
     assert out.cpu().tolist()[0] == 0
+
+
+def test_concurrent_callers(cuda, oracle):
+    """Host API called from several threads at once (the reference's kernels are
+    nogil and thread-safe): every thread's streams and values stay exact."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import paper_2407_15037_b200 as g
+    from paper_2407_15037_b200 import workloads
+
+    xs = [workloads.c2_values((1 << 23) + 4096 * i + i) for i in range(4)]
+    refs = [oracle.compress(x, "rel", 1e-2, workers=4)[0] for x in xs]
+
+    def job(i):
+        out = []
+        for _ in range(3):
+            s, _ = g.compress(xs[i], _cfg("rel", 1e-2, 32))
+            y = g.decompress_to_array(s)
+            out.append((s == refs[i], np.array_equal(y.view(np.uint32),
+                                                     oracle.decompress_to_array(refs[i]).view(np.uint32))))
+        return out
+
+    with ThreadPoolExecutor(4) as ex:
+        for res in ex.map(job, range(4)):
+            assert all(a and b for a, b in res)
