@@ -77,31 +77,6 @@ def advise_hugepages(addr: int, n: int) -> None:
         _madvise(lo, hi - lo, _MADV_HUGEPAGE)
 
 
-_MADV_POPULATE_WRITE = 23
-
-
-def populate_async(addr: int, n: int, nthreads: int = 8) -> list:
-    """Fault in [addr, addr + n) ahead of use, in background threads.
-
-    madvise(MADV_POPULATE_WRITE) allocates the (zeroed) pages without writing
-    user data, so it may run concurrently with copies into the same range.
-    The page faults of a fresh multi-hundred-MB result otherwise serialise
-    behind the copies that first touch them.  Returns the threads (join them).
-    """
-    if _madvise is None or n < (8 << 20):
-        return []
-    lo = (addr + 4095) & ~4095
-    hi = (addr + n) & ~4095
-    step = max(((hi - lo) // nthreads + (2 << 20) - 1) & ~((2 << 20) - 1), 2 << 20)
-    ths = []
-    for a in range(lo, hi, step):
-        th = threading.Thread(target=_madvise, args=(a, min(step, hi - a), _MADV_POPULATE_WRITE),
-                              daemon=True)
-        th.start()
-        ths.append(th)
-    return ths
-
-
 def new_bytes(n: int):
     """An uninitialised bytes object of length n and a writable uint8 CPU tensor over it."""
     b = _PyBytes_FromStringAndSize(None, n)

@@ -192,35 +192,18 @@ def compress_pipelined(arr: np.ndarray, cfg: QuantConfig, header: StreamHeader):
         _d2h_ring_copy(ring, out_stream, enc_ev[c], src_dev, dst, state)
         state["base"] = base + L
 
-    populate = []
-
-    def prefault():
-        # size the result from the first span's compression and fault its pages
-        # in while the rest of the input is still crossing PCIe
-        enc_ev[0].synchronize()
-        v0, v1 = spans[0]
-        est = hdr_len + int(int(rl_host[0]) * (n / (v1 - v0)) * 1.1) + (4 << 20)
-        nth = int(os.environ.get("GEBQ_B200_PREFAULT_THREADS", "0"))
-        if nth > 0:
-            populate.extend(hostio.populate_async(out.addr, min(est, out.cap), nth))
-
     if pipe.pinned:          # every span's copy and encode queued at once
         for c in range(len(spans)):
             launch(c)
-        prefault()
         for c in range(len(spans)):
             drain(c)
     else:                    # staging copies interleave with draining the previous span
         for c in range(len(spans)):
             launch(c)
-            if c == 0:
-                prefault()
             if c:
                 drain(c - 1)
         drain(len(spans) - 1)
     _d2h_ring_flush(ring, state)
-    for th in populate:
-        th.join()
     total = state["base"]
     # index: span-relative entries -> stream offsets
     if nblocks:
