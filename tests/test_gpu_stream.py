@@ -277,6 +277,8 @@ def test_rel_filter_exhaustive(cuda, eb, unsafe):
     ("abs", 1e-3, 4096, True, 3 * (1 << 23) + 77),
     ("rel", 1e-2, 1000, False, 5 * (1 << 22) + 3),
     ("rel", 1e-3, 4096, True, 1 << 24),
+    ("noa", 1e-4, 65536, False, (1 << 23) + 12345),
+    ("abs", 1e-2, 1, True, (1 << 21) + 7),
 ])
 def test_pipelined_compress_vs_oracle(cuda, oracle, mode, eb, bs, pinned, n, monkeypatch):
     """Large inputs take the span-pipelined compress (PCIe overlapped with the
@@ -294,8 +296,9 @@ def test_pipelined_compress_vs_oracle(cuda, oracle, mode, eb, bs, pinned, n, mon
         t = torch.empty(n, dtype=torch.int32, pin_memory=True)
         t.numpy()[:] = x.view(np.int32)
         x = t.numpy().view(np.float32)
-    s, st = g.compress(x, QuantConfig(mode=mode, eb=eb, width=32, block_size=bs))
-    so, trig, _ = oracle.compress(x, mode, eb, block_size=bs, workers=8)
+    vr = 3.0 if mode == "noa" else None   # a pinned range: constants known up front
+    s, st = g.compress(x, QuantConfig(mode=mode, eb=eb, width=32, block_size=bs, value_range=vr))
+    so, trig, _ = oracle.compress(x, mode, eb, value_range=vr, block_size=bs, workers=8)
     assert len(s) == len(so)
     assert s == so
     assert trig_list(st.triggers) == list(trig)
