@@ -448,3 +448,27 @@ def test_concurrent_callers(cuda, oracle):
     with ThreadPoolExecutor(4) as ex:
         for res in ex.map(job, range(4)):
             assert all(a and b for a, b in res)
+
+
+@pytest.mark.parametrize("width", [32, 64])
+@pytest.mark.parametrize("offset", [1, 3])
+def test_stream_encode_misaligned_device_view(cuda, oracle, width, offset):
+    """A device view that is not 16 B aligned cannot be bulk-copied: the encoder
+    falls back to per-value loads; the stream (and its decode) must not change."""
+    import torch
+
+    import paper_2407_15037_b200 as g
+    from paper_2407_15037_b200 import device, stream
+
+    bits = mixed_bits(width, 5 * 4096 + 777, 13)
+    x = device.to_device(bits)
+    view = x[offset:]
+    cfg = _cfg("rel", 1e-2, width)
+    enc = stream.encode(view, cfg)
+    s = stream.stream_to_host(enc, stream.header_for(cfg, view.numel()))
+    ft = np.float32 if width == 32 else np.float64
+    so, _, _ = oracle.compress(bits[offset:].view(ft), "rel", 1e-2)
+    assert s == so
+    y = g.decompress_to_array(s)
+    np.testing.assert_array_equal(y.view(bits.dtype), oracle.decompress_to_array(so).view(bits.dtype))
+    torch.cuda.synchronize()
