@@ -472,3 +472,20 @@ def test_stream_encode_misaligned_device_view(cuda, oracle, width, offset):
     y = g.decompress_to_array(s)
     np.testing.assert_array_equal(y.view(bits.dtype), oracle.decompress_to_array(so).view(bits.dtype))
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("width", [32, 64])
+@pytest.mark.parametrize("mode,eb", [("abs", 1e-3), ("rel", 1e-2), ("noa", 1e-3)])
+def test_unsafe_streams_vs_oracle(cuda, oracle, width, mode, eb):
+    """unsafe_no_double_check streams (header flag bit 0; no double-check, so
+    bound violations are possible by design) equal the oracle byte for byte."""
+    import paper_2407_15037_b200 as g
+
+    ft = np.float32 if width == 32 else np.float64
+    x = mixed_bits(width, 3 * 4096 + 555, 17).view(ft)
+    s, st = g.compress(x, _cfg(mode, eb, width, unsafe=True))
+    so, trig, _ = oracle.compress(x, mode, eb, unsafe=True)
+    assert s == so
+    assert trig_list(st.triggers) == list(trig)
+    np.testing.assert_array_equal(g.decompress_to_array(s).view(np.uint8),
+                                  oracle.decompress_to_array(so).view(np.uint8))
