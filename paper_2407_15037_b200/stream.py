@@ -15,6 +15,7 @@ import ctypes
 import os
 import struct
 import threading
+import time
 from dataclasses import dataclass
 from typing import Optional
 
@@ -184,6 +185,8 @@ def compress_pipelined(arr: np.ndarray, cfg: QuantConfig, header: StreamHeader):
 
     def drain(c):
         enc_ev[c].synchronize()
+        if _TRACE is not None:
+            _TRACE.append((f"enc{c} done", time.perf_counter()))
         L = int(rl_host[c])
         base = state["base"]
         bases.append(base)
@@ -214,9 +217,13 @@ def compress_pipelined(arr: np.ndarray, cfg: QuantConfig, header: StreamHeader):
     prefix = header.pack() + struct.pack("<Q", nblocks)
     out.view[:len(prefix)].copy_(torch.frombuffer(bytearray(prefix), dtype=torch.uint8))
     trig_h = trig.cpu().numpy()
-    return out.finish(hdr_len + total), trig_h
+    r = out.finish(hdr_len + total)
+    if _TRACE is not None:
+        _TRACE.append(("finished", time.perf_counter()))
+    return r, trig_h
 
 
+_TRACE = None               # optional list of (event, perf_counter) for host-timeline probes
 _LOCAL = threading.local()   # per-thread staging rings / streams (concurrent callers never share)
 
 
@@ -243,7 +250,11 @@ def _d2h_ring_copy(ring, stream, after: torch.cuda.Event, src: torch.Tensor, dst
         if len(pend) == 2:                     # the slot about to be reused: finish its host copy
             pk, pdst, pm = pend.pop(0)
             evs[pk].synchronize()
+            if _TRACE is not None:
+                _TRACE.append((f"slot{pk} dma done", time.perf_counter()))
             pdst.copy_(slots[pk][:pm])
+            if _TRACE is not None:
+                _TRACE.append((f"slot{pk} host copy done", time.perf_counter()))
         with torch.cuda.stream(stream):
             slots[k][:m].copy_(src[off:off + m], non_blocking=True)
         evs[k].record(stream)
@@ -254,7 +265,11 @@ def _d2h_ring_flush(ring, state):
     slots, evs = ring
     for pk, pdst, pm in state.pop("pend", []):
         evs[pk].synchronize()
+        if _TRACE is not None:
+            _TRACE.append((f"slot{pk} dma done (flush)", time.perf_counter()))
         pdst.copy_(slots[pk][:pm])
+        if _TRACE is not None:
+            _TRACE.append((f"slot{pk} host copy done (flush)", time.perf_counter()))
 
 
 def encode_coded(codes: torch.Tensor, lossless: torch.Tensor, block_size: int, *,
