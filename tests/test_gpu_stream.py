@@ -489,3 +489,29 @@ def test_unsafe_streams_vs_oracle(cuda, oracle, width, mode, eb):
     assert trig_list(st.triggers) == list(trig)
     np.testing.assert_array_equal(g.decompress_to_array(s).view(np.uint8),
                                   oracle.decompress_to_array(so).view(np.uint8))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode,eb", [("rel", 1e-1), ("rel", 1e-2), ("rel", 1e-4), ("rel", 1e-6),
+                                     ("abs", 1e-3), ("abs", 1.0), ("abs", 1e30)])
+def test_decode_reconstruct_code_ranges_vs_oracle(cuda, oracle, mode, eb):
+    """Arbitrary codes through the fused decoder: every fast-path range bound of
+    reconstruct (the REL code limit derived from w, the small-int conversion
+    bounds) and the codes just across it must decode like the oracle."""
+    import paper_2407_15037_b200 as g
+
+    c = oracle.derive(mode, eb, 32)
+    d = c["header"]
+    rng = np.random.default_rng(11)
+    edges = [1 << 22, 1 << 23, 1 << 24, 1 << 25, 0xFFFFFFFF]
+    if mode == "rel":
+        K = int(np.float32(120.0) / np.float32(d))
+        edges += [4 * K, 4 * min(K, 1 << 22)]
+    pts = np.concatenate([np.arange(max(e - 16, 0), e + 16, dtype=np.int64) for e in edges]) & 0xFFFFFFFF
+    codes = np.concatenate([pts, rng.integers(0, 1 << 26, 20000), rng.integers(0, 1 << 32, 4000),
+                            np.arange(0, 4096)]).astype(np.uint32)
+    lossless = rng.random(codes.size) < 0.05
+    s = oracle.encode_stream(codes, lossless.view(np.uint8), mode, 32, eb, int(np.asarray(d).view(np.uint32)))
+    got = g.decompress_to_array(s).view(np.uint32)
+    exp = oracle.decompress_to_array(s).view(np.uint32)
+    np.testing.assert_array_equal(got, exp)
