@@ -505,8 +505,9 @@ def test_decode_reconstruct_code_ranges_vs_oracle(cuda, oracle, mode, eb):
     rng = np.random.default_rng(11)
     edges = [1 << 22, 1 << 23, 1 << 24, 1 << 25, 0xFFFFFFFF]
     if mode == "rel":
-        K = int(np.float32(120.0) / np.float32(d))
-        edges += [4 * K, 4 * min(K, 1 << 22)]
+        K = int(np.float32(125.9) / np.float32(d))
+        edges += [4 * K, 4 * min(K, (1 << 22) - 1)]
+        edges += [int(2 * (126.0 / float(d))) * 2, int(2 * (128.0 / float(d))) * 2]
     pts = np.concatenate([np.arange(max(e - 16, 0), e + 16, dtype=np.int64) for e in edges]) & 0xFFFFFFFF
     codes = np.concatenate([pts, rng.integers(0, 1 << 26, 20000), rng.integers(0, 1 << 32, 4000),
                             np.arange(0, 4096)]).astype(np.uint32)
