@@ -61,7 +61,7 @@ __device__ __forceinline__ void flush_trig(uint32_t t0, uint32_t t1, uint32_t t2
 // replaces quantize_{abs,rel}{32,64} (_kernels.py:86-285)
 // ---------------------------------------------------------------------------
 template <typename T, int kMode, bool kUnsafe>
-__global__ void __launch_bounds__(kThreads) k_quantize(const typename W<T>::U *__restrict__ x,
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 5 : 3) k_quantize(const typename W<T>::U *__restrict__ x,
                                                        typename W<T>::U *__restrict__ codes,
                                                        uint8_t *__restrict__ flags, int64_t n,
                                                        Consts<T> k, const Consts<T> *kdev,
@@ -75,16 +75,21 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename W<T>::U *_
         if constexpr (sizeof(T) == 4) ef = make_rel_exact(k);
     }
     // binary32 REL: the exact-division quantizer of the stream encoder whenever w
-    // is in its range (uniform); the filtered one otherwise
-    auto qv = [&](typename W<T>::U xb, typename W<T>::U &c) -> int {
-        if constexpr (kMode == MODE_REL && sizeof(T) == 4) {
-            if (ef.wdiv) return quantize_rel_exact32<kUnsafe>(xb, k, ef, c);
+    // is in its range (uniform); the filtered one otherwise.  The trigger comes
+    // back as a packed 5-bit counter increment (trig_inc; 0 = none).
+    auto qv = [&](typename W<T>::U xb, typename W<T>::U &c) -> uint32_t {
+        if constexpr (kMode == MODE_REL) {
+            if constexpr (sizeof(T) == 4) {
+                if (ef.wdiv) return (uint32_t)quantize_rel_exact32<kUnsafe, true>(xb, k, ef, c);
+            }
+            return trig_inc(quantize_bf<T, kMode, kUnsafe>(xb, k, f, c));
+        } else {
+            return (uint32_t)quantize_abs_bf<T, kUnsafe, true>(xb, k, c);
         }
-        return quantize_bf<T, kMode, kUnsafe>(xb, k, f, c);
     };
     uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
-    auto count = [&](int tr) {
-        c0 += tr == TRIG_NAN; c1 += tr == TRIG_INF; c2 += tr == TRIG_GUARD; c3 += tr == TRIG_DCHECK;
+    auto drain = [&](uint32_t tc) {   // at most 16 increments per 5-bit field
+        c0 += tc & 31u; c1 += (tc >> 5) & 31u; c2 += (tc >> 10) & 31u; c3 += (tc >> 15) & 31u;
     };
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t ntiles = vec_ok ? n / kTile : 0;
@@ -93,30 +98,32 @@ __global__ void __launch_bounds__(kThreads) k_quantize(const typename W<T>::U *_
         U v[kRows][4];
 #pragma unroll
         for (int r = 0; r < kRows; r++) Vec4<U>::load(x + base + 128 * r, v[r]);
+        uint32_t tc = 0;
 #pragma unroll
         for (int r = 0; r < kRows; r++) {
             uint32_t fl = 0;
 #pragma unroll
             for (int s = 0; s < 4; s++) {
                 U c;
-                int tr = qv(v[r][s], c);
+                const uint32_t inc = qv(v[r][s], c);
                 v[r][s] = c;
-                fl |= (uint32_t)(tr != TRIG_NONE) << (8 * s);
-                count(tr);
+                fl |= (uint32_t)(inc != 0u) << (8 * s);
+                tc += inc;
             }
             Vec4<U>::store(codes + base + 128 * r, v[r]);
             __stcs(reinterpret_cast<uint32_t *>(flags + base + 128 * r), fl);
         }
+        drain(tc);
     }
     // scalar tail (or everything when the pointers are not 16 B aligned)
     const int64_t start = ntiles * kTile;
     for (int64_t i = start + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         U c;
-        int tr = qv(x[i], c);
+        const uint32_t inc = qv(x[i], c);
         codes[i] = c;
-        flags[i] = tr != TRIG_NONE;
-        count(tr);
+        flags[i] = inc != 0u;
+        drain(inc);
     }
     flush_trig(c0, c1, c2, c3, trig);
 }
@@ -131,6 +138,13 @@ __global__ void __launch_bounds__(kThreads) k_reconstruct(const typename W<T>::U
                                                           int64_t n, T derived, int vec_ok) {
     using U = typename W<T>::U;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // binary32: the decode hot loop's reconstruct (exact fast ranges, the plain
+    // restatement reconstruct_one outside them)
+    const RelDec32 rd = make_rel_dec32(sizeof(T) == 4 && kMode == MODE_REL ? (float)derived : 0.0f);
+    auto rec = [&](U c, uint32_t fl) -> U {
+        if constexpr (sizeof(T) == 4) return reconstruct32_fast<kMode>(c, fl != 0u, derived, rd);
+        else return reconstruct_one<T, kMode>(c, fl != 0u, derived);
+    };
     const int64_t ntiles = vec_ok ? n / kTile : 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t base = tile * kTile + warp * (kTile / kWarps) + 4 * lane;
@@ -145,14 +159,14 @@ __global__ void __launch_bounds__(kThreads) k_reconstruct(const typename W<T>::U
         for (int r = 0; r < kRows; r++) {
 #pragma unroll
             for (int s = 0; s < 4; s++)
-                v[r][s] = reconstruct_one<T, kMode>(v[r][s], (fl[r] >> (8 * s)) & 0xFF, derived);
+                v[r][s] = rec(v[r][s], (fl[r] >> (8 * s)) & 0xFFu);
             Vec4<U>::store(out + base + 128 * r, v[r]);
         }
     }
     const int64_t start = ntiles * kTile;
     for (int64_t i = start + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = reconstruct_one<T, kMode>(codes[i], flags[i] != 0, derived);
+        out[i] = rec(codes[i], flags[i]);
 }
 
 // ---------------------------------------------------------------------------
@@ -371,15 +385,14 @@ int launch_quantize(int mode, const void *x, void *codes, uint8_t *flags, int64_
                     unsigned long long *trig, cudaStream_t st) {
     using U = typename W<T>::U;
     int vec = aligned16(x) && aligned16(codes) && aligned16(flags);
-    int grid = grid_for(n);
     auto *xp = (const U *)x;
     auto *cp = (U *)codes;
     if (mode == MODE_REL) {
-        if (unsafe) k_quantize<T, MODE_REL, true><<<grid, kThreads, 0, st>>>(xp, cp, flags, n, k, kdev, trig, vec);
-        else k_quantize<T, MODE_REL, false><<<grid, kThreads, 0, st>>>(xp, cp, flags, n, k, kdev, trig, vec);
+        if (unsafe) k_quantize<T, MODE_REL, true><<<grid_per_sm(n, 16), kThreads, 0, st>>>(xp, cp, flags, n, k, kdev, trig, vec);
+        else k_quantize<T, MODE_REL, false><<<grid_per_sm(n, 16), kThreads, 0, st>>>(xp, cp, flags, n, k, kdev, trig, vec);
     } else {
-        if (unsafe) k_quantize<T, MODE_ABS, true><<<grid, kThreads, 0, st>>>(xp, cp, flags, n, k, kdev, trig, vec);
-        else k_quantize<T, MODE_ABS, false><<<grid, kThreads, 0, st>>>(xp, cp, flags, n, k, kdev, trig, vec);
+        if (unsafe) k_quantize<T, MODE_ABS, true><<<grid_per_sm(n, 16), kThreads, 0, st>>>(xp, cp, flags, n, k, kdev, trig, vec);
+        else k_quantize<T, MODE_ABS, false><<<grid_per_sm(n, 16), kThreads, 0, st>>>(xp, cp, flags, n, k, kdev, trig, vec);
     }
     return check_launch("quantize");
 }
@@ -393,11 +406,10 @@ int launch_reconstruct(int mode, const void *codes, const uint8_t *flags, void *
                        T derived, cudaStream_t st) {
     using U = typename W<T>::U;
     int vec = aligned16(codes) && aligned16(out) && aligned16(flags);
-    int grid = grid_for(n);
     if (mode == MODE_REL)
-        k_reconstruct<T, MODE_REL><<<grid, kThreads, 0, st>>>((const U *)codes, flags, (U *)out, n, derived, vec);
+        k_reconstruct<T, MODE_REL><<<grid_tiles(n), kThreads, 0, st>>>((const U *)codes, flags, (U *)out, n, derived, vec);
     else
-        k_reconstruct<T, MODE_ABS><<<grid, kThreads, 0, st>>>((const U *)codes, flags, (U *)out, n, derived, vec);
+        k_reconstruct<T, MODE_ABS><<<grid_tiles(n), kThreads, 0, st>>>((const U *)codes, flags, (U *)out, n, derived, vec);
     return check_launch("reconstruct");
 }
 template int launch_reconstruct<float>(int, const void *, const uint8_t *, void *, int64_t, float, cudaStream_t);
@@ -414,8 +426,7 @@ int launch_noa_minmax(const void *x, int64_t n, long long *keys2, cudaStream_t s
         e = cudaMemcpyAsync(keys2, none, sizeof(none), cudaMemcpyHostToDevice, st);
         if (e != cudaSuccess) return set_error(e, "noa init");
     }
-    int grid = grid_for(n);
-    k_noa_minmax<T><<<grid, kThreads, 0, st>>>((const U *)x, n, keys2, aligned16(x));
+    k_noa_minmax<T><<<grid_per_sm(n, 8), kThreads, 0, st>>>((const U *)x, n, keys2, aligned16(x));
     return check_launch("noa_minmax");
 }
 template int launch_noa_minmax<float>(const void *, int64_t, long long *, cudaStream_t);
@@ -632,9 +643,8 @@ int launch_verify(int rel, const void *o, const void *r, int64_t n, T bound, uns
                   uint8_t *mask, cudaStream_t st) {
     using U = typename W<T>::U;
     if (n <= 0) return 0;
-    const int grid = grid_for(n);
-    if (rel) k_verify<T, true><<<grid, kThreads, 0, st>>>((const U *)o, (const U *)r, n, bound, out5, mask);
-    else k_verify<T, false><<<grid, kThreads, 0, st>>>((const U *)o, (const U *)r, n, bound, out5, mask);
+    if (rel) k_verify<T, true><<<grid_per_sm(n, 8), kThreads, 0, st>>>((const U *)o, (const U *)r, n, bound, out5, mask);
+    else k_verify<T, false><<<grid_per_sm(n, 8), kThreads, 0, st>>>((const U *)o, (const U *)r, n, bound, out5, mask);
     return check_launch("verify");
 }
 template int launch_verify<float>(int, const void *, const void *, int64_t, float, unsigned long long *, uint8_t *,

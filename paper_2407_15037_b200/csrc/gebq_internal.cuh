@@ -35,6 +35,24 @@ inline int grid_for(int64_t n) {
     if (tiles < 1) tiles = 1;
     return (int)(tiles < g ? tiles : g);
 }
+// grid of at most one full wave of Kern (its measured residency per SM, not the
+// 2048-thread ideal): a grid-stride loop over a second, partial wave leaves SMs
+// idle for a whole CTA lifetime
+// Grids of the elementwise kernels, measured on B200 (C2 / C5 CodedArray stage):
+// reconstruct streams best as one CTA per 4096-value tile
+// (the block scheduler keeps every SM fed to the end; a resident-sized grid
+// was 17 % slower), quantize best with 16 CTAs per SM oversubscribed (its
+// register-limited residency is 5 CTAs; one exact wave was 6 % slower)
+inline int grid_tiles(int64_t n) {
+    const int64_t tiles = (n + kTile - 1) / kTile;
+    return (int)(tiles < 1 ? 1 : tiles < (1 << 30) ? tiles : (1 << 30));
+}
+inline int grid_per_sm(int64_t n, int per_sm) {
+    int64_t tiles = (n + kTile - 1) / kTile;
+    const int64_t g = (int64_t)sm_count() * per_sm;
+    if (tiles < 1) tiles = 1;
+    return (int)(tiles < g ? tiles : g);
+}
 
 template <typename T>
 int launch_quantize(int mode, const void *x, void *codes, uint8_t *flags, int64_t n,
