@@ -14,4 +14,8 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 40 --cs
   python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch_c2.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_encode4k_sp|k_decode4k_sp" -s 2 -c 2 \
   -o gpurun_out/prof_c2_full python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full_c2.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_quantize|k_reconstruct" -c 2 \
+  -o gpurun_out/prof_c2_coded python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_coded_c2.log 2>&1
+timeout 900 compute-sanitizer --tool memcheck python -m pytest tests -m gpu -q -k "not sweep and not exhaustive" \
+  > gpurun_out/memcheck_gpu.log 2>&1
 exit 0
