@@ -2,6 +2,7 @@
 // declarations shared by the kernel files and the C-ABI (capi.cu).
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -28,6 +29,24 @@ bool force_generic_kernels();
 
 // SM count x resident CTAs of kThreads (queried once per device)
 int sm_count();
+
+// Raise Kern's dynamic shared memory limit to at least `smem` on the current
+// device (the attribute belongs to the per-device module, so it is tracked per
+// device; concurrent callers may both set it, which is harmless).  0 or the
+// set_error code.
+template <auto Kern>
+inline int ensure_dyn_smem(int smem, const char *what) {
+    static std::atomic<int> done[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+    if (smem <= 48 * 1024 || done[dev].load(std::memory_order_acquire) >= smem) return 0;
+    const cudaError_t e = cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return set_error(e, what);
+    int cur = done[dev].load(std::memory_order_relaxed);
+    while (cur < smem && !done[dev].compare_exchange_weak(cur, smem, std::memory_order_release)) {
+    }
+    return 0;
+}
 int resident_grid();
 inline int grid_for(int64_t n) {
     int64_t tiles = (n + kTile - 1) / kTile;

@@ -666,12 +666,7 @@ size_t encode_workspace_bytes(int64_t n, int64_t bs, int width) {
 template <typename T, int kSrc, int kMode, bool kUnsafe>
 static int encode_dispatch(const EncodeCfg &cfg, EncArgs<T> a, int smem, int grid, cudaStream_t st) {
     auto kern = k_encode<T, kSrc, kMode, kUnsafe>;
-    static int configured_smem = 0;  // per-instantiation attribute cache
-    if (smem > 48 * 1024 && smem > configured_smem) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return set_error(e, "encode smem attribute");
-        configured_smem = smem;
-    }
+    if (int rc = ensure_dyn_smem<k_encode<T, kSrc, kMode, kUnsafe>>(smem, "encode smem attribute")) return rc;
     kern<<<grid, kThreads, smem, st>>>(a);
     return check_launch("encode");
 }
@@ -790,12 +785,7 @@ static int decode_dispatch(const DecodeCfg &d, const uint8_t *region, const int6
         const int buf_bytes = (int)((bmb + d.block_size * maxl + 1 + 16 + 15) / 16 * 16);
         const int smem = buf_bytes + (int)(d.block_size * 2);
         auto kern = k_decode_par<T, kSink, kMode>;
-        static int configured = 0;
-        if (smem > 48 * 1024 && smem > configured) {
-            cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            if (e != cudaSuccess) return set_error(e, "decode smem attribute");
-            configured = smem;
-        }
+        if (int rc = ensure_dyn_smem<k_decode_par<T, kSink, kMode>>(smem, "decode smem attribute")) return rc;
         int per_sm = (200 * 1024) / (smem + 2048);
         if (per_sm > 2048 / kThreads) per_sm = 2048 / kThreads;
         if (per_sm < 1) per_sm = 1;
