@@ -365,6 +365,37 @@ def test_encoder_image_sizes_vs_oracle(cuda, oracle, kind):
         assert trig_list(st.triggers) == list(trig)
 
 
+@pytest.mark.parametrize("kind", ["nan", "mixed_len", "random", "zeros"])
+def test_encoder_f64_image_sizes_vs_oracle(cuda, oracle, kind):
+    """binary64 tile images from 1-byte to 10-byte varints: the full-tile word
+    emission (up to three word stores per code, the first word of each run merged
+    by the previous run after the barrier) and the byte path of the partial last
+    tile; streams must equal the oracle."""
+    import paper_2407_15037_b200 as g
+
+    rng = np.random.default_rng(12)
+    n = (1 << 21) + 777
+    if kind == "nan":       # lossless NaN payloads, sign set: every code 10 bytes
+        bits = rng.integers(0, 1 << 51, n, dtype=np.uint64) | np.uint64(0xFFF0000000000001)
+    elif kind == "mixed_len":   # ABS bins of every magnitude: varint lengths 1..10 at every alignment
+        mag = rng.integers(-12, 62, n)
+        vals = np.ldexp(rng.random(n) + 0.5, mag) * np.where(rng.random(n) < 0.5, -1.0, 1.0)
+        vals[rng.random(n) < 0.05] = np.nan
+        bits = vals.view(np.uint64)
+    elif kind == "random":
+        bits = rng.integers(0, 1 << 63, n, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, n, dtype=np.uint64)
+    else:
+        bits = np.zeros(n, np.uint64)
+    x = bits.view(np.float64)
+    for mode, eb in (("abs", 1e-3), ("rel", 1e-2)):
+        s, st = g.compress(x, _cfg(mode, eb, 64))
+        so, trig, _ = oracle.compress(x, mode, eb, workers=8)
+        assert s == so, (kind, mode)
+        assert trig_list(st.triggers) == list(trig)
+        np.testing.assert_array_equal(g.decompress_to_array(s).view(np.uint8),
+                                      oracle.decompress_to_array(so, workers=8).view(np.uint8))
+
+
 @pytest.mark.parametrize("width,mode", [(32, "rel"), (32, "abs"), (64, "abs")])
 def test_decode_fuzz_multiblock_vs_oracle(cuda, oracle, width, mode):
     """Byte mutations of 33-block streams (whole-block bulk copies, edge blocks,
