@@ -38,20 +38,43 @@ sys.path.insert(0, ROOT)
 METRIC = "quantize/dequantize GB/s at 1/2/4/8 B200 vs HBM roofline; 0 bound violations"
 
 WORKLOADS = {
+    "c3": dict(desc="C3: NOA f32 eb=1e-4, 1024^3 smooth field (2^30 values, counter-based noise, planted "
+                    "NaN/+Inf/-7/+7) sharded over the GPUs",
+               mode="noa", eb=1e-4, width=32, n=1 << 30, scaling="strong", cpu_sample=1 << 26),
     "c2": dict(desc="C2: REL f32 eb=1e-2, mixed NaN/Inf/denormal/huge (SURVEY App. C), 2^26 values per GPU",
-               mode="rel", eb=1e-2, width=32, n=1 << 26, scaling="weak"),
+               mode="rel", eb=1e-2, width=32, n=1 << 26, scaling="weak", cpu_sample=1 << 26),
     "c1": dict(desc="C1: ABS f32 eb=1e-3, 256^3 smooth field per GPU", mode="abs", eb=1e-3,
-               width=32, n=1 << 24, scaling="weak"),
-    "c3": dict(desc="C3: NOA f32 eb=1e-4, 1024^3 smooth field (2^30 values) sharded over the GPUs",
-               mode="noa", eb=1e-4, width=32, n=1 << 30, scaling="strong"),
-    "c5": dict(desc="C5: ABS f64 eb=1e-3, 2^28 random splitmix64 doubles per GPU", mode="abs",
-               eb=1e-3, width=64, n=1 << 28, scaling="weak"),
-    "c5rel": dict(desc="C5: REL f64 eb=1e-3, 2^28 random splitmix64 doubles per GPU", mode="rel",
-                  eb=1e-3, width=64, n=1 << 28, scaling="weak"),
+               width=32, n=1 << 24, scaling="weak", cpu_sample=1 << 24),
+    "c5": dict(desc="C5: ABS f64 eb=1e-3, 2^30 random splitmix64 doubles per GPU", mode="abs",
+               eb=1e-3, width=64, n=1 << 30, scaling="weak", cpu_sample=1 << 25),
+    "c5rel": dict(desc="C5: REL f64 eb=1e-3, 2^30 random splitmix64 doubles per GPU", mode="rel",
+                  eb=1e-3, width=64, n=1 << 30, scaling="weak", cpu_sample=1 << 25),
+    "c5s": dict(desc="C5: ABS f64 eb=1e-3, 2^30-value smooth field (1024^3, counter-based noise) per GPU",
+                mode="abs", eb=1e-3, width=64, n=1 << 30, scaling="weak", cpu_sample=1 << 25),
+    "c5rels": dict(desc="C5: REL f64 eb=1e-3, 2^30-value smooth field (1024^3, counter-based noise) per GPU",
+                   mode="rel", eb=1e-3, width=64, n=1 << 30, scaling="weak", cpu_sample=1 << 25),
     "c4": dict(desc="C4: exhaustive sweep of all 2^32 f32 patterns through ABS 1e-3, REL 1e-2 and "
                     "NOA 1e-4 (R=1), pattern range sharded over the GPUs", mode="sweep", eb=None,
                width=32, n=1 << 32, scaling="strong"),
 }
+
+
+def shard_size(wl: dict, world: int) -> int:
+    return wl["n"] // world if wl["scaling"] == "strong" else wl["n"]
+
+
+def config_dict(wl: dict, world: int, args) -> dict:
+    """The config both arms print (identical keys and values for the same flags)."""
+    n = shard_size(wl, world)
+    W = wl["width"] // 8
+    cfg = {"workload": wl["desc"], "n_per_gpu": n, "n_total": n * world, "block_size": 4096,
+           "parallelism": f"dp{world} (contiguous block-aligned shards)",
+           "l2": "inputs larger than L2 (values %d MiB per GPU)" % (n * W >> 20),
+           "gbs_basis": "uncompressed bytes encoded + decoded per second, all GPUs"}
+    if getattr(args, "unsafe", False):
+        cfg["unsafe_no_double_check"] = True
+    return cfg
+
 
 # SURVEY Appendix B: exhaustive 2^32 tallies (normal class quantized / lossless)
 C4_CONFIGS = (("abs", 1e-3, None, 2443713898, 1817698966),
@@ -65,7 +88,9 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
+    ap.add_argument("--unsafe", action="store_true",
+                    help="skip the double-check (the paper's 'unprotected' quantizer, PAPER.md:428-441)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -171,11 +196,7 @@ def make_input(wl: dict, name: str, rank: int, world: int, device):
     from paper_2407_15037_b200 import device as gdev
     from paper_2407_15037_b200 import workloads
 
-    if wl["scaling"] == "strong":
-        n_total = wl["n"]
-        n = n_total // world
-    else:
-        n = wl["n"]
+    n = shard_size(wl, world)
     start = rank * n
     if name == "c2":
         return gdev.mixed_f32(n, workloads.C2_SEED, start, device=device), n
@@ -185,28 +206,12 @@ def make_input(wl: dict, name: str, rank: int, world: int, device):
         x = workloads.smooth_field(256, rank, np.float32)
         return torch.from_numpy(x.view(np.int32)).to(device), n
     if name == "c3":
-        # 1024^3 smooth field in f64 math, cast once; noise from the CUDA Philox
-        # generator (seed 1) -- both GPU and CPU checkers consume these same bits.
-        side = 1024
-        g = torch.Generator(device=device)
-        g.manual_seed(1 + rank)
-        idx = torch.arange(start, start + n, device=device, dtype=torch.int64)
-        i = (idx // (side * side)).double()
-        j = ((idx // side) % side).double()
-        k = (idx % side).double()
-        two_pi = 2 * np.pi
-        x = (5.0 * torch.sin(two_pi * i / side) * torch.cos(two_pi * j / side)
-             * torch.sin(two_pi * k / (side // 2)))
-        x = x + 0.02 * torch.randn(n, generator=g, device=device, dtype=torch.float64)
-        x = x.float()
-        if rank == 0:
-            x[0] = float("nan")
-            x[1] = float("inf")
-            x[2] = -7.0
-        if rank == world - 1:
-            x[-1] = 7.0
-        del i, j, k, idx
-        return x.view(torch.int32), n
+        # counter-based field of the GLOBAL index: identical bits at every world size
+        return gdev.smooth_field(n, workloads.C3_SIDE, workloads.C3_SEED, start, 32, plant=True,
+                                 total=wl["n"], device=device), n
+    if name in ("c5s", "c5rels"):
+        return gdev.smooth_field(n, workloads.C3_SIDE, workloads.C5_SMOOTH_SEED, start, 64, plant=False,
+                                 device=device), n
     raise ValueError(name)
 
 
@@ -214,20 +219,26 @@ def make_input(wl: dict, name: str, rank: int, world: int, device):
 # reference arm / CPU baseline: the oracle port on the host cores
 # ---------------------------------------------------------------------------
 def host_input(name: str, wl: dict, n: int) -> np.ndarray:
+    """The first n values of rank 0's shard, built on the host by the same recipes
+    (bit-identical to ``make_input``; tests/test_gpu_workloads.py checks it)."""
     from paper_2407_15037_b200 import workloads
 
     if name == "c2":
         return workloads.c2_values(n)
     if name in ("c5", "c5rel"):
-        return workloads.c5_random_values(n)
+        return workloads.splitmix64(n, workloads.C5_SEED).view(np.float64)
     if name == "c1":
-        return workloads.smooth_field(256, 0, np.float32)
+        return workloads.smooth_field(256, 0, np.float32)[:n]
     if name == "c3":
-        return workloads.plant_noa_extremes(workloads.smooth_field(1024, 1, np.float32))[:n]
+        return workloads.smooth_field_cb(n, workloads.C3_SIDE, workloads.C3_SEED, 0, np.float32,
+                                         plant=True, total=wl["n"])
+    if name in ("c5s", "c5rels"):
+        return workloads.smooth_field_cb(n, workloads.C3_SIDE, workloads.C5_SMOOTH_SEED, 0, np.float64,
+                                         plant=False)
     raise ValueError(name)
 
 
-def cpu_roundtrip_gbs(x: np.ndarray, wl: dict, workers: int, reps: int):
+def cpu_roundtrip_gbs(x: np.ndarray, wl: dict, workers: int, reps: int, unsafe: bool = False):
     """Median GB/s (same basis) of oracle compress + decompress on the host cores."""
     from oracle import oracle as orc
 
@@ -235,7 +246,7 @@ def cpu_roundtrip_gbs(x: np.ndarray, wl: dict, workers: int, reps: int):
     times = []
     for _ in range(reps):
         t0 = time.perf_counter()
-        s, _, _ = orc.compress(x, wl["mode"], wl["eb"], workers=workers)
+        s, _, _ = orc.compress(x, wl["mode"], wl["eb"], unsafe=unsafe, workers=workers)
         y = orc.decompress_to_array(s, workers=workers)
         times.append(time.perf_counter() - t0)
         del s, y
@@ -244,34 +255,37 @@ def cpu_roundtrip_gbs(x: np.ndarray, wl: dict, workers: int, reps: int):
 
 
 def run_reference(args, wl, name):
+    """--impl reference: the reference algorithm (oracle/ C port of gebq's numba
+    loops) on all host threads; each step compresses + decompresses a bounded
+    sample (the first ``cpu_sample`` values of rank 0's shard) of the workload."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
-    n = wl["n"] if wl["scaling"] == "weak" else wl["n"]
+    n = min(shard_size(wl, world), wl["cpu_sample"])
     cores = os.cpu_count() or 1
     x = host_input(name, wl, n)
     from oracle import oracle as orc
 
     orc.lib()
     for _ in range(max(args.warmup, 1)):
-        s, _, _ = orc.compress(x, wl["mode"], wl["eb"], workers=cores)
+        s, _, _ = orc.compress(x, wl["mode"], wl["eb"], unsafe=args.unsafe, workers=cores)
         orc.decompress_to_array(s, workers=cores)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        s, _, _ = orc.compress(x, wl["mode"], wl["eb"], workers=cores)
+        s, _, _ = orc.compress(x, wl["mode"], wl["eb"], unsafe=args.unsafe, workers=cores)
         orc.decompress_to_array(s, workers=cores)
         times.append(time.perf_counter() - t0)
     t = float(np.mean(times))
     value = 2 * x.nbytes / t / 1e9
-    sample = f"full {name} batch ({n} values, {x.nbytes} B) per step, compress + decompress"
+    sample = (f"first {n} values ({x.nbytes >> 20} MiB) of rank 0's {name} shard per step, "
+              f"compress + decompress on {cores} threads")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None,
         "dtype": "f32" if wl["width"] == 32 else "f64", "data": "synthetic",
-        "config": {"workload": wl["desc"], "n": n, "block_size": 4096,
-                   "gbs_basis": "uncompressed bytes encoded + decoded per second"},
+        "config": config_dict(wl, world, args),
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -295,6 +309,12 @@ def _expected_tally(mode, q, l):
         t[0, 0], t[1, 0] = 2, 16777214   # zero / denormal: quantized
     t[2, 0], t[2, 1] = q, l
     return t
+
+
+def sweep_config(wl: dict, world: int) -> dict:
+    return {"workload": wl["desc"], "patterns_total": 1 << 32,
+            "parallelism": f"dp{world} (contiguous pattern ranges)",
+            "gbs_basis": "4 B per pattern x 3 configurations per step"}
 
 
 def run_sweep_bench(args, wl):
@@ -327,7 +347,7 @@ def run_sweep_bench(args, wl):
                 "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (all f32 bit patterns)",
-                "config": {"workload": wl["desc"], "sample": f"3 x 2^27 patterns from 0x3F000000 per step"},
+                "config": sweep_config(wl, world),
                 "patterns_per_s": pps,
                 "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port",
                                  "sample": "3 configs x 2^27 consecutive patterns per step"},
@@ -417,9 +437,7 @@ def run_sweep_bench(args, wl):
         line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (all 2^32 f32 bit patterns, generated in-kernel)",
-                "config": {"workload": wl["desc"], "patterns_per_gpu": count,
-                           "parallelism": f"dp{world} (contiguous pattern ranges)",
-                           "gbs_basis": "4 B per pattern x 3 configurations per step"},
+                "config": sweep_config(wl, world), "patterns_per_gpu": count,
                 "patterns_per_s": pps, "violations": violations, "tallies_match_appendix_b": bool(match),
                 "e2e": {"value": e2e, "unit": "GB/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 3 * 16 * 8,
@@ -462,7 +480,7 @@ def main():
 
     x, n = make_input(wl, args.workload, rank, world, dev)
     W = wl["width"] // 8
-    cfg = QuantConfig(mode=wl["mode"], eb=wl["eb"], width=wl["width"])
+    cfg = QuantConfig(mode=wl["mode"], eb=wl["eb"], width=wl["width"], unsafe_no_double_check=args.unsafe)
     bs = cfg.block_size
     nblocks = -(-n // bs)
     buf = stream.alloc_stream(n, bs, wl["width"], dev)
@@ -611,7 +629,8 @@ def main():
         pinned = torch.empty(n, dtype=x.dtype, pin_memory=True)
         pinned.copy_(x)
         xh = pinned.numpy().view(ft)
-        e2e_cfg = QuantConfig(mode=wl["mode"], eb=wl["eb"], width=wl["width"])
+        e2e_cfg = QuantConfig(mode=wl["mode"], eb=wl["eb"], width=wl["width"],
+                              unsafe_no_double_check=args.unsafe)
         # warm-up with the timed loop's exact allocation pattern (the previous
         # step's stream and values stay alive while the next step allocates)
         s = y = None
@@ -642,11 +661,12 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
-        xh_cpu = host_input(args.workload, wl, n)
-        gbs, tmed, times = cpu_roundtrip_gbs(xh_cpu, wl, cores, reps=5)
+        m = min(n, wl["cpu_sample"])
+        xh_cpu = x[:m].cpu().numpy().view(np.float32 if wl["width"] == 32 else np.float64)  # same bits
+        gbs, tmed, times = cpu_roundtrip_gbs(xh_cpu, wl, cores, reps=5, unsafe=args.unsafe)
         cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port",
-               "sample": f"full {args.workload} batch ({n} values) compress+decompress, median of 5 "
-                         f"({tmed * 1e3:.0f} ms each) on {cores} threads"}
+               "sample": f"first {m} values of the GPU arm's input (same bits), compress+decompress, "
+                         f"median of 5 ({tmed * 1e3:.0f} ms each) on {cores} threads"}
 
     if rank == 0:
         line = {
@@ -654,11 +674,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": wl["scaling"], "vs_baseline": None,
             "dtype": "f32" if wl["width"] == 32 else "f64", "data": "synthetic",
-            "config": {"workload": wl["desc"], "n_per_gpu": n, "block_size": bs,
-                       "parallelism": f"dp{world} (contiguous block-aligned shards)",
-                       "l2": "inputs larger than L2 (values %d MiB, stream %d MiB per GPU)" % (
-                           n * W >> 20, stream_bytes >> 20),
-                       "gbs_basis": "uncompressed bytes encoded + decoded per second, all GPUs"},
+            "config": config_dict(wl, world, args),
             "e2e": e2e,
             "roofline": {"bound": "hbm", "kernel": dominant[0], "achieved": dominant[3],
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",

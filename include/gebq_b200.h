@@ -134,6 +134,17 @@ int gebq_splitmix64_fill(uint64_t *out, int64_t n, uint64_t seed, int64_t start_
                          void *stream);
 int gebq_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_index,
                        void *stream);
+/* gen_smooth: the C3 / C5-smooth field with counter-based noise (bench and
+ * parity workloads; no reference counterpart -- the reference's synthetic
+ * field, bench.py:357-374, draws numpy noise that a GPU cannot reproduce).
+ * g = start_index + i, (ii, j, k) = digits of g in base side;
+ * v = ((5*tab3[ii]) * tab3[side+j]) * tab3[2*side+k] + (s - 131070) * noise_scale
+ * in binary64 (one rounding each), s = sum of the four 16-bit fields of
+ * splitmix64(seed, g+1); out = v (width 64) or (float)v (width 32).  plant:
+ * g=0 NaN, g=1 +Inf, g=2 -7, g=total-1 +7.  tab3 is a device array.        */
+int gebq_gen_smooth(int width, void *out, int64_t n, int64_t side, const double *tab3,
+                    uint64_t seed, int64_t start_index, int plant, int64_t total,
+                    double noise_scale, void *stream);
 
 
 /* ---- library-log REL variant: quantize_rel32_lib / reconstruct_rel32_lib
@@ -251,6 +262,21 @@ int gebq_selfcheck_abs_f32(uint64_t start, int64_t count, float eb_eff, float eb
                            int unsafe, unsigned long long *out2, void *stream);
 int gebq_selfcheck_rel_filter_f32(uint64_t start, int64_t count, float op_eps, float w, float thr,
                                   int unsafe, unsigned long long *out2, void *stream);
+/* Self-check of the production binary64 quantizers (the stream encoder's and
+ * CodedArray kernel's ABS op sequence and filtered REL quantizer) against the
+ * reference op sequences (quantize_abs64 _kernels.py:126-162, quantize_rel64
+ * :227-285) over `count` sampled patterns from splitmix64(seed): raw words,
+ * moderate magnitudes, bin / double-check edges and range edges (see
+ * k_check_f64).  out2[0] += mismatching (code, trigger) outcomes -- must stay
+ * 0; out2[1] += patterns checked.                                           */
+int gebq_selfcheck_abs_f64(uint64_t seed, int64_t count, double eb_eff, double eb2, double inv_eb2,
+                           double thr, int unsafe, unsigned long long *out2, void *stream);
+int gebq_selfcheck_rel_f64(uint64_t seed, int64_t count, double op_eps, double w, double thr, int unsafe,
+                           unsigned long long *out2, void *stream);
+/* The binary32 REL encoder's FCHK-free division against div.rn for any
+ * bound w in [2^-100, 2^100] (sampled (l, w) pairs and double-check
+ * quotients).  out2[0] += differing quotients; out2[1] += pairs checked.    */
+int gebq_selfcheck_div_f32(uint64_t seed, int64_t count, unsigned long long *out2, void *stream);
 
 /* decode_span_*: the fused decode restricted to blocks [b0, b1) of a stream
  * (same region / offsets / count as the whole-stream call; outputs land at

@@ -52,6 +52,7 @@ SIGNATURES = {
     "gebq_sweep_rel_f64": [_int, _vp, _u64, _i64, _u64, _f64, _f64, _f64, _int, _vp, _vp, _vp],
     "gebq_splitmix64_fill": [_vp, _i64, _u64, _i64, _vp],
     "gebq_gen_mixed_f32": [_vp, _i64, _u64, _i64, _vp],
+    "gebq_gen_smooth": [_int, _vp, _i64, _i64, _vp, _u64, _i64, _int, _i64, _f64, _vp],
     "gebq_quantize_rel_lib_f32": [_vp, _vp, _vp, _i64, _f32, _f32, _f32, _int, _vp, _vp],
     "gebq_dequantize_rel_lib_f32": [_vp, _vp, _vp, _i64, _f32, _vp],
     "gebq_verify_f32": [_vp, _vp, _i64, _int, _f32, _vp, _vp, _vp],
@@ -83,6 +84,9 @@ SIGNATURES = {
     "gebq_decode_span_rel_f64": [_vp, _i64, _vp, _i64, _i64, _i64, _f64, _i64, _i64, _vp, _vp, _vp],
     "gebq_selfcheck_abs_f32": [_u64, _i64, _f32, _f32, _f32, _f32, _int, _vp, _vp],
     "gebq_selfcheck_rel_filter_f32": [_u64, _i64, _f32, _f32, _f32, _int, _vp, _vp],
+    "gebq_selfcheck_abs_f64": [_u64, _i64, _f64, _f64, _f64, _f64, _int, _vp, _vp],
+    "gebq_selfcheck_rel_f64": [_u64, _i64, _f64, _f64, _f64, _int, _vp, _vp],
+    "gebq_selfcheck_div_f32": [_u64, _i64, _vp, _vp],
     "gebq_decode_blocks_u32": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp],
     "gebq_decode_blocks_u64": [_vp, _vp, _i64, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp],
     "gebq_block_sizes_u32": [_vp, _i64, _i64, _i64, _i64, _vp, _vp],

@@ -180,6 +180,11 @@ int gebq_splitmix64_fill(uint64_t *out, int64_t n, uint64_t seed, int64_t start_
 int gebq_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_index, void *stream) {
     return launch_gen_mixed_f32(out, n, seed, start_index, S(stream));
 }
+int gebq_gen_smooth(int width, void *out, int64_t n, int64_t side, const double *tab3, uint64_t seed,
+                    int64_t start_index, int plant, int64_t total, double noise_scale, void *stream) {
+    if ((width != 32 && width != 64) || side <= 0 || n < 0) return set_error_msg(-1, "gen_smooth: bad arguments");
+    return launch_gen_smooth(width, out, n, side, tab3, seed, start_index, plant, total, noise_scale, S(stream));
+}
 int gebq_quantize_rel_lib_f32(const uint32_t *x, uint32_t *codes, uint8_t *lossless, int64_t n, float op_eps,
                               float w, float thr, int unsafe, unsigned long long *trig4, void *stream) {
     return launch_rel32_lib_quantize(x, codes, lossless, n, op_eps, w, thr, unsafe, trig4, S(stream));
@@ -359,6 +364,20 @@ int gebq_selfcheck_rel_filter_f32(uint64_t start, int64_t count, float op_eps, f
                                   int unsafe, unsigned long long *out2, void *stream) {
     Consts<float> k{op_eps, w, 0.0f, thr};
     return launch_check_rel_try(start, count, k, unsafe, out2, S(stream));
+}
+
+int gebq_selfcheck_abs_f64(uint64_t seed, int64_t count, double eb_eff, double eb2, double inv_eb2, double thr,
+                           int unsafe, unsigned long long *out2, void *stream) {
+    Consts<double> k{eb_eff, eb2, inv_eb2, thr};
+    return launch_check_f64(MODE_ABS, seed, count, k, unsafe, out2, S(stream));
+}
+int gebq_selfcheck_rel_f64(uint64_t seed, int64_t count, double op_eps, double w, double thr, int unsafe,
+                           unsigned long long *out2, void *stream) {
+    Consts<double> k{op_eps, w, 0.0, thr};
+    return launch_check_f64(MODE_REL, seed, count, k, unsafe, out2, S(stream));
+}
+int gebq_selfcheck_div_f32(uint64_t seed, int64_t count, unsigned long long *out2, void *stream) {
+    return launch_check_div32(seed, count, out2, S(stream));
 }
 
 int gebq_decode_blocks_u32(const uint8_t *buf, const int64_t *offsets, int64_t noffsets, int64_t region_end,

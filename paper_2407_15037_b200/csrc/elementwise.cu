@@ -376,6 +376,36 @@ __global__ void k_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t
     }
 }
 
+// C3 / C5-smooth field (workloads.smooth_field_cb): counter-based, so every
+// shard of every world size and the host recipe produce identical bits.
+//   g = start + i;  k = g % side, j = (g / side) % side, ii = (g / side^2) % side
+//   w = splitmix64(seed, g + 1); s = sum of w's four 16-bit fields (exact)
+//   v = ((5 * A[ii]) * B[j]) * C[k] + (s - 131070) * nz   (f64, one rounding each)
+// planted (NOA range test): g = 0 NaN, 1 +Inf, 2 -7, total - 1 +7.
+template <typename T>
+__global__ void k_gen_smooth(T *out, int64_t n, int64_t side, const double *__restrict__ tab,
+                             uint64_t seed, int64_t start_index, int plant, int64_t total, double nz) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t g = start_index + i;
+        int64_t k = g % side, j = (g / side) % side, ii = (g / side / side) % side;
+        uint64_t w = splitmix64_at(seed, (uint64_t)g + 1);
+        int64_t s = (int64_t)(w & 0xFFFF) + (int64_t)((w >> 16) & 0xFFFF) + (int64_t)((w >> 32) & 0xFFFF) +
+                    (int64_t)(w >> 48);
+        double noise = __dmul_rn((double)(s - 131070), nz);
+        double v = __dmul_rn(__dmul_rn(__dmul_rn(5.0, tab[ii]), tab[side + j]), tab[2 * side + k]);
+        v = __dadd_rn(v, noise);
+        if (plant) {
+            if (g == 0) v = __longlong_as_double(0x7FF8000000000000ll);
+            else if (g == 1) v = __longlong_as_double(0x7FF0000000000000ll);
+            else if (g == 2) v = -7.0;
+            else if (g == total - 1) v = 7.0;
+        }
+        if constexpr (sizeof(T) == 4) out[i] = __double2float_rn(v);
+        else out[i] = v;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // host launchers (called from capi.cu)
 // ---------------------------------------------------------------------------
@@ -415,17 +445,19 @@ int launch_reconstruct(int mode, const void *codes, const uint8_t *flags, void *
 template int launch_reconstruct<float>(int, const void *, const uint8_t *, void *, int64_t, float, cudaStream_t);
 template int launch_reconstruct<double>(int, const void *, const uint8_t *, void *, int64_t, double, cudaStream_t);
 
+// key "none" (no finite value seen): 0 for the f32 keys (max taken as unsigned
+// 32-bit), INT64_MIN for the signed-int64 view of the f64 keys.  Written by a
+// kernel, not a pageable host copy, so the range pass stays graph-capturable.
+__global__ void k_noa_init(long long *keys2, long long none) {
+    if (threadIdx.x < 2) keys2[threadIdx.x] = none;
+}
+
 template <typename T>
 int launch_noa_minmax(const void *x, int64_t n, long long *keys2, cudaStream_t st) {
     using U = typename W<T>::U;
-    cudaError_t e = cudaMemsetAsync(keys2, 0, 2 * sizeof(long long), st);
-    if (e != cudaSuccess) return set_error(e, "noa memset");
-    if constexpr (sizeof(T) == 8) {
-        // "none" for the signed-int64 view of f64 keys is INT64_MIN
-        static const long long none[2] = {(long long)0x8000000000000000ull, (long long)0x8000000000000000ull};
-        e = cudaMemcpyAsync(keys2, none, sizeof(none), cudaMemcpyHostToDevice, st);
-        if (e != cudaSuccess) return set_error(e, "noa init");
-    }
+    k_noa_init<<<1, 32, 0, st>>>(keys2, sizeof(T) == 8 ? (long long)0x8000000000000000ull : 0ll);
+    int rc = check_launch("noa_init");
+    if (rc) return rc;
     k_noa_minmax<T><<<grid_per_sm(n, 8), kThreads, 0, st>>>((const U *)x, n, keys2, aligned16(x));
     return check_launch("noa_minmax");
 }
@@ -489,6 +521,17 @@ int64_t sweep_per_launch() { return (int64_t)resident_grid() * kThreads * 60000;
 int launch_splitmix64_fill(uint64_t *out, int64_t n, uint64_t seed, int64_t start_index, cudaStream_t st) {
     k_splitmix64_fill<<<grid_for(n), kThreads, 0, st>>>(out, n, seed, start_index);
     return check_launch("splitmix64_fill");
+}
+int launch_gen_smooth(int width, void *out, int64_t n, int64_t side, const double *tab, uint64_t seed,
+                      int64_t start_index, int plant, int64_t total, double nz, cudaStream_t st) {
+    if (n <= 0) return 0;
+    if (width == 32)
+        k_gen_smooth<float><<<grid_for(n), kThreads, 0, st>>>((float *)out, n, side, tab, seed, start_index, plant,
+                                                               total, nz);
+    else
+        k_gen_smooth<double><<<grid_for(n), kThreads, 0, st>>>((double *)out, n, side, tab, seed, start_index,
+                                                                plant, total, nz);
+    return check_launch("gen_smooth");
 }
 int launch_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_index, cudaStream_t st) {
     k_gen_mixed_f32<<<grid_for(n), kThreads, 0, st>>>(out, n, seed, start_index);

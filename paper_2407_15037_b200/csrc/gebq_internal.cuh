@@ -98,6 +98,8 @@ int launch_rel32_lib_reconstruct(const uint32_t *codes, const uint8_t *flags, ui
                                  cudaStream_t st);
 int launch_splitmix64_fill(uint64_t *out, int64_t n, uint64_t seed, int64_t start_index,
                            cudaStream_t st);
+int launch_gen_smooth(int width, void *out, int64_t n, int64_t side, const double *tab, uint64_t seed,
+                      int64_t start_index, int plant, int64_t total, double nz, cudaStream_t st);
 int launch_gen_mixed_f32(uint32_t *out, int64_t n, uint64_t seed, int64_t start_index,
                          cudaStream_t st);
 

@@ -56,6 +56,9 @@ template <typename T>
 int launch_decode4k(const DecodeCfg &d, const uint8_t *region, const int64_t *offsets, T derived,
                     void *out_codes, uint8_t *out_flags, unsigned long long *err_key, cudaStream_t st);
 
+int launch_check_f64(int mode, uint64_t seed, int64_t count, const Consts<double> &k, int unsafe,
+                     unsigned long long *out2, cudaStream_t st);
+int launch_check_div32(uint64_t seed, int64_t count, unsigned long long *out2, cudaStream_t st);
 int launch_check_abs_bf(uint64_t start, int64_t count, const Consts<float> &k, int unsafe,
                         unsigned long long *out2, cudaStream_t st);
 int launch_check_rel_try(uint64_t start, int64_t count, const Consts<float> &k, int unsafe,

@@ -209,6 +209,21 @@ def mixed_f32(n: int, seed: int, start_index: int = 0, device=None) -> torch.Ten
     return out
 
 
+def smooth_field(n: int, side: int, seed: int, start_index: int = 0, width: int = 32,
+                 plant: bool = True, total: Optional[int] = None, device=None) -> torch.Tensor:
+    """Counter-based C3 / C5-smooth field (``workloads.smooth_field_cb``) as an
+    int32 / int64 bit tensor, generated on the device from the global index."""
+    from . import workloads
+
+    dev = require_cuda(device)
+    total = side ** 3 if total is None else total
+    tab = torch.from_numpy(workloads.smooth_tables(side).reshape(-1).copy()).to(dev)
+    out = torch.empty(n, dtype=_ITYPE[width], device=dev)
+    _lib.call("gebq_gen_smooth", width, _p(out), n, side, _p(tab), seed & (2 ** 64 - 1), start_index,
+              int(bool(plant)), total, workloads.SMOOTH_NOISE_SCALE, _s())
+    return out
+
+
 # ---------------------------------------------------------------------------
 # host conveniences (numpy in / numpy out) used by the drop-in shims
 # ---------------------------------------------------------------------------

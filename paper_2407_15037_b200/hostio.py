@@ -219,20 +219,54 @@ class H2DPipe:
 # --- a bytes result built in place, sized after the fact -------------------
 # PyBytes_FromStringAndSize(NULL, cap) creates an uninitialised object owned by
 # the caller (refcount 1); _PyBytes_Resize shrinks such a brand-new object to
-# its final length (the documented way to build a bytes whose size is only
-# known at the end; realloc of the large block shrinks in place).  Only the
-# touched pages of the capacity are ever backed by memory.
-_bytes_new_raw = ctypes.PYFUNCTYPE(ctypes.c_void_p, ctypes.c_char_p, ctypes.c_ssize_t)(
-    ("PyBytes_FromStringAndSize", ctypes.pythonapi))
-_bytes_as_string = ctypes.PYFUNCTYPE(ctypes.c_void_p, ctypes.c_void_p)(("PyBytes_AsString", ctypes.pythonapi))
-_bytes_resize = ctypes.PYFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), ctypes.c_ssize_t)(
-    ("_PyBytes_Resize", ctypes.pythonapi))
-_py_decref = ctypes.pythonapi.Py_DecRef
-_py_decref.argtypes = [ctypes.c_void_p]
-_py_decref.restype = None
+# its final length (the C-API way to build a bytes whose size is only known at
+# the end; realloc of the large block shrinks in place).  Only the touched
+# pages of the capacity are ever backed by memory.  _PyBytes_Resize is private
+# CPython API: it is used only on a GIL-enabled CPython 3.8-3.13 that exports
+# it; anywhere else the builder falls back to a bytearray + one final copy.
+def _resize_supported() -> bool:
+    import sys
+    import sysconfig
+
+    if sys.implementation.name != "cpython" or not (3, 8) <= sys.version_info[:2] <= (3, 13):
+        return False
+    if sysconfig.get_config_var("Py_GIL_DISABLED"):
+        return False
+    return hasattr(ctypes.pythonapi, "_PyBytes_Resize") and hasattr(ctypes.pythonapi, "PyBytes_AsString")
 
 
-class BytesBuilder:
+RESIZE_IN_PLACE = _resize_supported()
+if RESIZE_IN_PLACE:
+    _bytes_new_raw = ctypes.PYFUNCTYPE(ctypes.c_void_p, ctypes.c_char_p, ctypes.c_ssize_t)(
+        ("PyBytes_FromStringAndSize", ctypes.pythonapi))
+    _bytes_as_string = ctypes.PYFUNCTYPE(ctypes.c_void_p, ctypes.c_void_p)(("PyBytes_AsString", ctypes.pythonapi))
+    _bytes_resize = ctypes.PYFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_void_p), ctypes.c_ssize_t)(
+        ("_PyBytes_Resize", ctypes.pythonapi))
+    _py_decref = ctypes.pythonapi.Py_DecRef
+    _py_decref.argtypes = [ctypes.c_void_p]
+    _py_decref.restype = None
+else:  # pragma: no cover - exercised through the fallback test
+    _py_decref = None
+
+
+class _BytearrayBuilder:
+    """Portable fallback: fill a bytearray, copy the used prefix out once."""
+
+    def __init__(self, cap: int):
+        self.cap = cap
+        self._buf = bytearray(cap)
+        self.view = torch.frombuffer(self._buf, dtype=torch.uint8) if cap else torch.empty(0, dtype=torch.uint8)
+
+    def finish(self, n: int) -> bytes:
+        if not 0 <= n <= self.cap:
+            raise ValueError("final length beyond capacity")
+        self.view = None
+        out = bytes(memoryview(self._buf)[:n])
+        self._buf = None
+        return out
+
+
+class _ResizeBuilder:
     """A new ``bytes`` of up to ``cap`` bytes, filled through a writable uint8 view
     and finalised with :meth:`finish` (which shrinks it to the used length)."""
 
@@ -263,3 +297,8 @@ class BytesBuilder:
             self.view = None
             _py_decref(obj)
             self._obj = ctypes.c_void_p(0)
+
+
+def BytesBuilder(cap: int):
+    """The in-place builder where the interpreter supports it, else the fallback."""
+    return _ResizeBuilder(cap) if RESIZE_IN_PLACE else _BytearrayBuilder(cap)

@@ -207,3 +207,41 @@ def test_plugin_install_rebinds_reference_operator_layer():
     for n in KERNEL_NAMES:
         assert getattr(ref_k, n) is before[n], n
     assert ref_p.compute_noa_range is cnr
+
+
+@pytest.mark.parametrize("in_place", [True, False])
+def test_bytes_builder_both_paths(monkeypatch, in_place):
+    """hostio.BytesBuilder: the _PyBytes_Resize path (where supported) and the
+    portable bytearray fallback give the same bytes."""
+    import torch
+
+    from paper_2407_15037_b200 import hostio
+
+    if in_place and not hostio.RESIZE_IN_PLACE:
+        pytest.skip("interpreter without _PyBytes_Resize")
+    monkeypatch.setattr(hostio, "RESIZE_IN_PLACE", in_place)
+    for cap, n in ((0, 0), (10, 7), (1 << 20, 12345), (5 << 20, 5 << 20)):
+        b = hostio.BytesBuilder(cap)
+        src = torch.arange(n, dtype=torch.int64).to(torch.uint8)
+        b.view[:n].copy_(src)
+        out = b.finish(n)
+        assert isinstance(out, bytes) and len(out) == n
+        assert out == bytes(src.numpy())
+    with pytest.raises(ValueError):
+        hostio.BytesBuilder(4).finish(5)
+
+
+def test_smooth_field_cb_recipe():
+    """Counter-based C3 field: chunking/offset invariant, planted extremes, R = 14."""
+    from paper_2407_15037_b200 import workloads as w
+
+    a = w.smooth_field_cb(50000, chunk=7777)
+    b = w.smooth_field_cb(20000, start_index=30000)
+    np.testing.assert_array_equal(a[30000:].view(np.uint32), b.view(np.uint32))
+    assert np.isnan(a[0]) and a[1] == np.inf and a[2] == -7.0
+    t = w.smooth_field_cb(8, start_index=(1 << 30) - 8, total=1 << 30)
+    assert t[-1] == 7.0
+    f = a[np.isfinite(a)]
+    assert f.min() == -7.0 and 0.01 < float(np.std(f[1:])) < 1.0
+    d = w.smooth_field_cb(1000, dtype=np.float64, plant=False)
+    assert np.all(np.isfinite(d)) and np.array_equal(d.astype(np.float32), w.smooth_field_cb(1000, plant=False)[:1000])
