@@ -89,6 +89,10 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c3")
+    ap.add_argument("--variant", choices=["fused", "lib"], default="fused",
+                    help="lib: the paper's approx-vs-library REL comparison (PAPER.md:366-386) -- the "
+                         "CodedArray quantize -> pack -> unpack -> reconstruct chain with the library-log "
+                         "kernels (_kernels.py:356-431) timed beside the same chain with the approx ones")
     ap.add_argument("--unsafe", action="store_true",
                     help="skip the double-check (the paper's 'unprotected' quantizer, PAPER.md:428-441)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -452,6 +456,89 @@ def run_sweep_bench(args, wl):
 
 
 # ---------------------------------------------------------------------------
+# --variant lib: approx vs library log2/exp2 REL (the paper's Tables 4/6/7)
+# ---------------------------------------------------------------------------
+def run_variant_bench(args, wl):
+    """REL f32 chain quantize -> pack -> unpack -> reconstruct, once with the
+    conforming approx kernels and once with the library-log ones
+    (quantize_rel32_lib / reconstruct_rel32_lib, non-conforming by design);
+    same input, same stages, same timing.  value = the lib chain's GB/s."""
+    import ctypes
+
+    import torch
+
+    from paper_2407_15037_b200 import _lib, device as gdev, stream
+    from paper_2407_15037_b200.container import StreamHeader
+    from paper_2407_15037_b200.quantizers import QuantConfig
+
+    if wl["mode"] != "rel" or wl["width"] != 32:
+        raise SystemExit("--variant lib needs a REL binary32 workload (the *_lib kernels are binary32)")
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    _lib.load()
+    x, n = make_input(wl, args.workload, rank, world, dev)
+    cfg = QuantConfig(mode="rel", eb=wl["eb"], width=32, unsafe_no_double_check=args.unsafe)
+    d = cfg.derived
+    st = torch.cuda.current_stream()
+    codes = torch.empty_like(x)
+    ll = torch.empty(n, dtype=torch.uint8, device=dev)
+    trig = torch.zeros(4, dtype=torch.int64, device=dev)
+    out = torch.empty_like(x)
+    hdr = StreamHeader(width=32, mode="rel", count=n, eb_bits=0, derived_bits=d.header_bits,
+                       block_size=cfg.block_size)
+    nblocks = -(-n // cfg.block_size)
+    P = ctypes.c_void_p
+
+    def chain(lib: bool):
+        if lib:
+            _lib.call("gebq_quantize_rel_lib_f32", P(x.data_ptr()), P(codes.data_ptr()), P(ll.data_ptr()), n,
+                      float(d.op_eps), float(d.w), float(d.thr), int(args.unsafe), P(trig.data_ptr()),
+                      P(st.cuda_stream))
+        else:
+            gdev.quantize(x, cfg, codes=codes, lossless=ll, trig=trig)
+        enc = stream.encode_coded(codes, ll, cfg.block_size)
+        c2, l2, _err = stream.decode_codes(enc.buf, hdr, nblocks)
+        if lib:
+            _lib.call("gebq_dequantize_rel_lib_f32", P(c2.data_ptr()), P(l2.data_ptr()), P(out.data_ptr()), n,
+                      float(d.w), P(st.cuda_stream))
+        else:
+            gdev.reconstruct(c2, l2, "rel", d.w, out=out)
+        return enc
+
+    res = {}
+    launches0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        for lib in (False, True):
+            for _ in range(args.warmup):
+                enc = chain(lib)
+            torch.cuda.synchronize()
+            rl = int(enc.region_len.item())
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record(st)
+            for _ in range(args.steps):
+                chain(lib)
+            t1.record(st)
+            torch.cuda.synchronize()
+            ms = t0.elapsed_time(t1) / args.steps
+            res["lib" if lib else "approx"] = {"ms_per_step": ms, "gbs": 2 * n * 4 / (ms * 1e-3) / 1e9,
+                                               "stream_bytes_per_value": (rl + 56 + 8 * nblocks) / n}
+    launches = _lib.launch_count() - launches0
+    line = {"metric": METRIC, "value": res["lib"]["gbs"], "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["lib"]["ms_per_step"], "higher_is_better": True,
+            "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": dict(config_dict(wl, world, args), variant="lib"),
+            "variant_compare": dict(res, lib_over_approx=res["lib"]["gbs"] / res["approx"]["gbs"],
+                                    ratio_loss_approx=res["approx"]["stream_bytes_per_value"]
+                                    / res["lib"]["stream_bytes_per_value"] - 1.0,
+                                    chain="CodedArray quantize -> pack -> unpack -> reconstruct (4 launches)"),
+            "clocks": clk.summary(), "gpu_launches": launches}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
 def main():
@@ -462,6 +549,8 @@ def main():
         return run_sweep_bench(args, wl)
     if args.impl == "reference":
         return run_reference(args, wl, args.workload)
+    if args.variant == "lib":
+        return run_variant_bench(args, wl)
 
     import torch
     import torch.distributed as dist

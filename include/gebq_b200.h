@@ -93,6 +93,15 @@ int gebq_dequantize_rel_f64(const uint64_t *codes, const uint8_t *lossless, uint
  *   range_out = (double)R.  Both outputs are device pointers.                */
 int gebq_noa_minmax_f32(const uint32_t *x, int64_t n, long long *keys2, void *stream);
 int gebq_noa_minmax_f64(const uint64_t *x, int64_t n, long long *keys2, void *stream);
+/* The one cross-GPU exchange of the path: in place
+ * ncclAllReduce(keys2, keys2, 2, ncclInt64, ncclMax, comm, stream) over the
+ * two order keys of gebq_noa_minmax_* ([key(max), ~key(min)], both "larger is
+ * more extreme"), so every rank then derives identical constants with
+ * gebq_noa_derive_*.  `nccl_comm` is an ncclComm_t of the caller's NCCL (the
+ * libnccl.so.2 loaded in the process is used; no link-time dependency).
+ * Replaces the global reduction implied by compute_noa_range over the whole
+ * array (quantizers.py:337-351) when the array is sharded.                  */
+int gebq_noa_allreduce(long long *keys2, void *nccl_comm, void *stream);
 int gebq_noa_derive_f32(const long long *keys2, double eb, void *consts_out, double *range_out,
                         void *stream);
 int gebq_noa_derive_f64(const long long *keys2, double eb, void *consts_out, double *range_out,

@@ -44,6 +44,7 @@ SIGNATURES = {
     "gebq_dequantize_rel_f64": [_vp, _vp, _vp, _i64, _f64, _vp],
     "gebq_noa_minmax_f32": [_vp, _i64, _vp, _vp],
     "gebq_noa_minmax_f64": [_vp, _i64, _vp, _vp],
+    "gebq_noa_allreduce": [_vp, _vp, _vp],
     "gebq_noa_derive_f32": [_vp, _f64, _vp, _vp, _vp],
     "gebq_noa_derive_f64": [_vp, _f64, _vp, _vp, _vp],
     "gebq_sweep_abs_f32": [_int, _vp, _u64, _i64, _u64, _f32, _f32, _f32, _f32, _int, _vp, _vp, _vp],

@@ -4,7 +4,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <mutex>
 #include <string>
+
+#include <dlfcn.h>
 
 #include "../../include/gebq_b200.h"
 #include "gebq_internal.cuh"
@@ -137,6 +140,37 @@ int gebq_noa_derive_f32(const long long *keys2, double eb, void *consts_out, dou
 int gebq_noa_derive_f64(const long long *keys2, double eb, void *consts_out, double *range_out,
                         void *stream) {
     return launch_noa_derive<double>(keys2, eb, (Consts<double> *)consts_out, range_out, S(stream));
+}
+
+// ---- NOA cross-GPU exchange ----------------------------------------------------
+// ncclAllReduce(keys2, keys2, 2, ncclInt64, ncclMax, comm, stream), resolved at
+// run time from the libnccl.so.2 already loaded in the process (the one that
+// created `comm`, e.g. torch's), else loaded here -- the library itself has
+// no link-time NCCL dependency.
+typedef int (*nccl_allreduce_t)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+typedef const char *(*nccl_errstr_t)(int);
+static nccl_allreduce_t g_nccl_allreduce = nullptr;
+static nccl_errstr_t g_nccl_errstr = nullptr;
+static std::once_flag g_nccl_once;
+
+int gebq_noa_allreduce(long long *keys2, void *nccl_comm, void *stream) {
+    std::call_once(g_nccl_once, [] {
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        g_nccl_allreduce = (nccl_allreduce_t)dlsym(h, "ncclAllReduce");
+        g_nccl_errstr = (nccl_errstr_t)dlsym(h, "ncclGetErrorString");
+    });
+    if (!g_nccl_allreduce) return set_error_msg(-1, "noa_allreduce: libnccl.so.2 not available");
+    if (!nccl_comm || !keys2) return set_error_msg(-1, "noa_allreduce: null communicator or keys");
+    const int kInt64 = 4, kMax = 2;   // ncclInt64, ncclMax (nccl.h)
+    int r = g_nccl_allreduce(keys2, keys2, 2, kInt64, kMax, nccl_comm, S(stream));
+    if (r != 0) {
+        std::string m = std::string("noa_allreduce: ncclAllReduce failed: ") +
+                        (g_nccl_errstr ? g_nccl_errstr(r) : "unknown NCCL error");
+        return set_error_msg(-1, m.c_str());
+    }
+    return 0;
 }
 
 // ---- sweeps -------------------------------------------------------------------
