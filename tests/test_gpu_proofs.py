@@ -141,3 +141,41 @@ def test_sweep_f64_appendix_b(cuda, mode):
     assert rep.violations == 0 and int(t[:, 2].sum()) == 0
     for ci, cls in enumerate(("zero", "denormal", "normal", "infinity", "nan")):
         assert (int(t[ci, 0]), int(t[ci, 1])) == F64_APPENDIX_B[mode][cls], (mode, cls)
+
+
+@pytest.mark.parametrize("mode,eb,vr,unsafe", [
+    ("abs", 1e-3, None, False), ("abs", 1e-3, None, True), ("abs", 1e-1, None, False),
+    ("abs", 1e-7, None, False), ("noa", 1e-4, 1.0, False), ("rel", 1e-2, None, False),
+])
+def test_stream_encoder_exhaustive_f32(cuda, mode, eb, vr, unsafe):
+    """Every f32 pattern through the fused stream encoder (k_encode4k_sp, whose
+    full-tile rows have their own fast quantize / length paths): the stream
+    decodes (k_decode4k_sp, codes sink) to exactly the codes and lossless flags
+    of the stand-alone quantizer k_quantize (itself proven against the
+    reference op sequence over all 2^32 patterns above), with equal trigger
+    counts.  Patterns enter in 16 chunks of 2^28, shuffled within each chunk by
+    a fixed bijection so every tile mixes magnitudes and signs."""
+    import torch
+
+    from paper_2407_15037_b200 import device as gdev, stream
+    from paper_2407_15037_b200.quantizers import QuantConfig
+
+    cfg = QuantConfig(mode=mode, eb=eb, width=32, value_range=vr, unsafe_no_double_check=unsafe)
+    n = 1 << 28
+    idx = torch.arange(n, dtype=torch.int64, device="cuda")
+    # odd multiplier mod 2^28: a bijection of the chunk; keep tiles of runs too
+    perm = (idx * 0x9E3779B1) & (n - 1)
+    hdr = stream.header_for(cfg, n)
+    nblocks = -(-n // cfg.block_size)
+    for c in range(16):
+        bits = ((perm if c % 2 else idx) + (c << 28)).to(torch.int32)
+        enc = stream.encode(bits, cfg)
+        rl = int(enc.region_len.item())
+        buf = enc.buf[:enc.region_off + rl]
+        codes, ll, err = stream.decode_codes(buf, hdr, nblocks)
+        q, qll, qtrig = gdev.quantize(bits, cfg)
+        assert int(err.item()) == -1, c
+        assert torch.equal(codes, q), c
+        assert torch.equal(ll, qll), c
+        assert enc.trig.cpu().tolist() == qtrig.cpu().tolist(), c
+        del enc, buf, codes, ll, q, qll
