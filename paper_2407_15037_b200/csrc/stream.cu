@@ -777,7 +777,9 @@ static int decode_dispatch(const DecodeCfg &d, const uint8_t *region, const int6
                            void *oc, uint8_t *of, unsigned long long *err, cudaStream_t st) {
     const int64_t nblk = d.b1 - d.b0;
     if (nblk <= 0) return 0;
-    if (d.block_size == kEncTileMax && !force_generic_kernels())
+    // the 4096-value kernel stores 128-bit value vectors (and 32-bit flag quads)
+    const bool vec_ok = aligned16(oc) && (kSink == 1 || ((uintptr_t)of & 3u) == 0);
+    if (d.block_size == kEncTileMax && vec_ok && !force_generic_kernels())
         return launch_decode4k<T>(d, region, offsets, derived, oc, of, err, st);
     if (d.block_size >= 64 && d.block_size <= kEncTileMax) {
         const int maxl = W<T>::kMaxVarint;
