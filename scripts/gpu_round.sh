@@ -19,10 +19,10 @@ for w in c3 c2 c5 c5rel; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_encode4k_sp|k_decode4k_sp" -s 2 -c 2 \
     -o gpurun_out/prof_${w}_full python bench.py --workload $w --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full_$w.log 2>&1
 done
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_quantize|k_reconstruct|k_noa_minmax" -c 3 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_quantize|k_reconstruct" -c 2 \
   -o gpurun_out/prof_c3_coded python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_coded_c3.log 2>&1
-timeout 1200 compute-sanitizer --tool memcheck python -m pytest tests -m gpu -q -k "not sweep and not exhaustive and not fullsize and not proofs" \
-  > gpurun_out/memcheck_gpu.log 2>&1
+timeout 1500 compute-sanitizer --tool memcheck python -m pytest tests/test_gpu_stream.py tests/test_gpu_elementwise.py -q \
+  -k "not exhaustive and not large and not fuzz_typed and not concurrent" > gpurun_out/memcheck_gpu.log 2>&1
 timeout 1200 compute-sanitizer --tool racecheck --racecheck-report hazard python -m pytest tests/test_gpu_stream.py -q \
   -k "golden or grid or image_sizes or fuzz_multiblock or code_ranges or misaligned or unsafe" > gpurun_out/racecheck_gpu.log 2>&1
 exit 0
