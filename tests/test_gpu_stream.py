@@ -547,3 +547,57 @@ def test_decode_reconstruct_code_ranges_vs_oracle(cuda, oracle, mode, eb):
     got = g.decompress_to_array(s).view(np.uint32)
     exp = oracle.decompress_to_array(s).view(np.uint32)
     np.testing.assert_array_equal(got, exp)
+
+
+def test_decode_fast_path_noncanonical(cuda, oracle):
+    """The binary32 table-driven parse of full blocks (<= 2-byte varints):
+    zeroing the terminator of a 2-byte varint (non-canonical) or of a 1-byte
+    varint's neighbour, at the start, middle and end of several blocks, gives
+    the oracle's error class and byte position."""
+    import re
+
+    import paper_2407_15037_b200 as g
+
+    n = 8 * 4096
+    i = np.arange(n, dtype=np.float64)
+    x = (np.sin(i * 1e-3) * 10.0).astype(np.float32)          # codes < 2^14: 1..2-byte varints
+    base, _ = g.compress(x, _cfg("abs", 1e-3, 32))
+    nb = 8
+    region0 = 56 + 8 * nb
+    offs = np.frombuffer(base, dtype="<u8", count=nb, offset=56)
+
+    def ours(data):
+        try:
+            return "OK:" + sha(g.decompress_to_array(data).tobytes())[:16]
+        except g.ContainerError as e:
+            m = re.search(r"byte (\d+)", str(e))
+            return type(e).__name__ + (":" + m.group(1) if m else "")
+
+    def ref(data):
+        try:
+            return "OK:" + sha(oracle.decompress_to_array(data).tobytes())[:16]
+        except oracle.DecodeError as e:
+            m = re.search(r"byte (\d+)", str(e))
+            return e.kind + (":" + m.group(1) if m else "")
+
+    assert ours(base) == ref(base)
+    checked = 0
+    for b in (0, 3, 7):
+        p = region0 + int(offs[b]) + 512                          # first varint of block b
+        ends = []                                                 # (first byte, last byte) per varint
+        while len(ends) < 4096:
+            q = p
+            while base[q] & 0x80:
+                q += 1
+            ends.append((p, q))
+            p = q + 1
+        two = [e for e in ends if e[1] == e[0] + 1]
+        assert len(two) > 8
+        for first, last in (two[0], two[len(two) // 2], two[-1]):
+            s = bytearray(base)
+            s[last] = 0x00                                        # non-canonical 2-byte varint
+            s = bytes(s)
+            r = ours(s)
+            assert r == ref(s) and not r.startswith("OK"), (b, last, r)
+            checked += 1
+    assert checked == 9
